@@ -1,0 +1,389 @@
+#!/usr/bin/env python
+"""Benchmark of the gridded-KDE hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--path auto|direct|tensor]
+    python bench.py --impl reference ...      # the fp64 CPU oracle on the host cores
+
+A step is one pass of the whole hot path over one batch of synthetic input that is
+already resident in HBM: kde_load_points (a1 convert/keys, a2 stable counting sort +
+gather, plan) followed by kde_eval (a3 direct or a4 tensor-core evaluation, a5 scale +
+store).  Under torchrun (N > 1) each rank owns a tile-aligned row band of the raster,
+bins the replicated point set with the band's halo filter, evaluates its band, and an
+NCCL all-gather assembles the heatmap (a6) inside the timed step.
+
+Metric (BASELINE.json): kernel evaluations per second = useful (pixel, point) pairs
+inside the support (kde_stats.useful_pairs, summed over bands) / step time; heatmap
+pixels/s is reported beside it.  Timing: W untimed warm-ups, then K steps, each
+preceded by an L2 flush (a 512 MiB write) outside its CUDA-event bracket; barrier +
+synchronize around the whole timed region; max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+# BASELINE.json configs -> concrete synthetic inputs
+CONFIGS = {
+    "C1": dict(preset="estuary", n=10_000, W=256, hpx=2.0, kernel="gaussian", cutoff=4.0, idx=0),
+    "C2": dict(preset="estuary", n=2_000_000, W=2048, hpx=4.0, kernel="gaussian", cutoff=4.0, idx=1),
+    "C3": dict(preset="promontory", n=5_000_000, W=4096, hpx=8.0, kernel="gaussian", cutoff=4.0, idx=2),
+    "C4": dict(preset="islands", n=20_000_000, W=8192, hpx=4.0, kernel="gaussian", cutoff=4.0, idx=3),
+}
+WORKLOAD = {
+    "C2": "South-Channel-Yangtze-Estuary-shaped 2M points, 2048x2048, Gaussian h=4px cutoff 4h",
+    "C1": "10k estuary points, 256x256, Gaussian h=2px cutoff 4h",
+    "C3": "Chengshan-Jiao-Promontory-shaped 5M points, 4096x4096, h=8px",
+    "C4": "Zhoushan-Islands-shaped 20M points, 8192x8192, Gaussian h=4px",
+}
+METRIC = "kernel evals/sec (useful pixel-point pairs) and heatmap pixels/sec"
+UNIT = "evals/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "sm_max_mhz": 1965.0}, "fallback"
+
+
+def _traffic(kernel_name):
+    """dram bytes/launch of the dominant kernel from the committed ncu capture, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(kernel_name)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.12)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[2 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def band_rows(H, ws, rank, tile=256):
+    """Equal tile-aligned row bands."""
+    from paper_2004_13653_b200.dist import plan_bands
+    return plan_bands(H, ws, tile)[rank]
+
+
+def _gen(cfg):
+    import aisgen
+    cloud = aisgen.generate(cfg["preset"], cfg["n"], aisgen.SEED_BASE + cfg["idx"])
+    x0, y0, res = aisgen.grid_for(cfg["preset"], cfg["W"])
+    return cloud, x0, y0, res
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2004_13653_b200 import KDE, KdeError
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = CONFIGS[args.config]
+    W = H = cfg["W"]
+    cloud, x0, y0, res = _gen(cfg)
+    rows = band_rows(H, ws, rank) if ws > 1 else (0, H)
+    nrows = rows[1] - rows[0]
+    k = KDE(x0, y0, res, W, H, cfg["hpx"] * res, kernel=cfg["kernel"], cutoff=cfg["cutoff"],
+            rows=rows if ws > 1 else None, device=local)
+    xd = torch.from_numpy(cloud.x).to(dev)
+    yd = torch.from_numpy(cloud.y).to(dev)
+    out = torch.empty((nrows, W), dtype=torch.float32, device=dev)
+    full = torch.empty((ws * nrows, W), dtype=torch.float32, device=dev) if ws > 1 else out
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    path = args.path
+    if path == "auto":
+        path = "tensor"
+        try:
+            k.load(xd, yd)
+            k.eval("tensor", out)
+        except KdeError:
+            path = "direct"
+
+    def step():
+        k.load(xd, yd)
+        k.eval(path, out)
+        if ws > 1:
+            dist.all_gather_into_tensor(full, out)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    st = k.stats()
+
+    # --- timed region: K steps, L2 flushed before each, events on the launching stream
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    launches0 = k.stats()["kernel_launches"]
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    launches = k.stats()["kernel_launches"] - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    ms = sum(step_ms) / len(step_ms)
+
+    # --- dominant kernel: eval alone (a3/a4 + a5), events on the same stream
+    evk = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.zero_()
+        evk[i][0].record(stream)
+        k.eval(path, out)
+        evk[i][1].record(stream)
+    torch.cuda.synchronize()
+    eval_ms = sum(a.elapsed_time(b) for a, b in evk) / args.steps
+
+    # --- e2e: same step through the public API with HOST buffers (pinned), incl. the
+    # H2D of the points and the D2H of the raster.
+    xh = torch.from_numpy(cloud.x).pin_memory()
+    yh = torch.from_numpy(cloud.y).pin_memory()
+    outh = torch.empty((nrows, W), dtype=torch.float32).pin_memory()
+    fullh = torch.empty((ws * nrows, W), dtype=torch.float32).pin_memory() if ws > 1 else outh
+
+    def step_e2e():
+        k.load(xh, yh)
+        k.eval(path, out)
+        if ws > 1:
+            dist.all_gather_into_tensor(full, out)
+            if rank == 0:
+                fullh.copy_(full, non_blocking=True)
+        else:
+            outh.copy_(out, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+
+    for _ in range(max(1, args.warmup // 2)):
+        step_e2e()
+    if ws > 1:
+        dist.barrier()
+    e2e_ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        step_e2e()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e = sum(e2e_ms) / len(e2e_ms)
+
+    # --- max over ranks; sum of units over ranks
+    useful = st["useful_pairs"]
+    vals = torch.tensor([ms, eval_ms, e2e, float(useful)], dtype=torch.float64, device=dev)
+    if ws > 1:
+        mx = vals.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = vals.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms, eval_ms, e2e = float(mx[0]), float(mx[1]), float(mx[2])
+        useful = int(sm[3])
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+
+    peaks, peak_src = _peaks()
+    clocks = clk.summary()
+    if path == "direct":
+        # ALU-bound: 1 FFMA (2 flops) per useful pair; FP32 peak = 148 SMs x 128 FFMA/clk
+        # x 2 flops x max SM clock
+        peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        roof = {"bound": "alu", "kernel": "direct_kernel<6,false>",
+                "achieved": 2.0 * st["useful_pairs"] / (eval_ms * 1e-3) / 1e12,
+                "peak": round(peak, 2), "unit": "TFLOP/s",
+                "peak_source": "derived: 148 SMs x 128 FP32 FMA/clk x 2 x sm_max_mhz (%s)" % peak_src}
+    else:
+        peak = peaks["bf16_tflops"]  # fp16 dense = bf16 dense rate (guide's nominal ratio 1)
+        roof = {"bound": "tensor", "kernel": "tc_gauss_kernel",
+                "achieved": 2.0 * st["useful_pairs"] / (eval_ms * 1e-3) / 1e12,
+                "peak": peak, "unit": "TFLOP/s",
+                "peak_source": f"{peak_src} bf16_tflops (fp16 dense rate = bf16)"}
+    roof["achieved"] = round(roof["achieved"], 3)
+    roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
+    roof["traffic"] = _traffic(roof["kernel"])
+    roof["eval_ms"] = round(eval_ms, 4)
+
+    line = {
+        "metric": METRIC, "value": useful / (ms * 1e-3), "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "strong" if ws > 1 else "weak",
+        "vs_baseline": None, "dtype": "f32" if path == "direct" else "f16xf16->f32",
+        "data": "synthetic (aisgen, seeded)",
+        "config": {"workload": WORKLOAD[args.config], "config": args.config, "path": path,
+                   "n_points": cfg["n"], "grid": f"{W}x{H}", "h_px": cfg["hpx"],
+                   "cutoff": cfg["cutoff"], "kernel": cfg["kernel"],
+                   "parallelism": f"row-bands x{ws}" if ws > 1 else "single",
+                   "l2": "flushed (512 MiB write) before every timed step"},
+        "pixels_per_s": W * H / (ms * 1e-3),
+        "useful_pairs": useful,
+        "e2e": {"value": useful / (e2e * 1e-3), "unit": UNIT, "ms_per_step": round(e2e, 4),
+                "h2d_bytes_per_step": 16 * cfg["n"],
+                "d2h_bytes_per_step": 4 * W * H},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "roofline": roof,
+    }
+    if not args.no_cpu_baseline and ws == 1:
+        line["cpu_baseline"] = cpu_baseline(cfg, cloud, x0, y0, res, args.cpu_seconds)
+    if ws > 1:
+        dist.destroy_process_group()
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(cfg, cloud, x0, y0, res, seconds=15.0):
+    """The oracle as it stands, timed on the host cores on a bounded sample: whole raster
+    rows (random, seeded), so the useful pairs in the sample are exact."""
+    import oracle
+    W = cfg["W"]
+    g = oracle.Grid(x0, y0, res, W, W, cfg["hpx"] * res, oracle.KERNELS.index(cfg["kernel"]),
+                    cfg["cutoff"])
+    cores = os.cpu_count() or 1
+    b = oracle.bin_points(g, 32, cloud.x, cloud.y)
+    rng_ = b["ranges"].astype(np.int64)
+    width = rng_[:, 1] - rng_[:, 0] + 1
+    rs = np.random.default_rng(7)
+    order = rs.permutation(W)
+    done_rows, pairs, t_used = 0, 0, 0.0
+    while t_used < seconds and done_rows < W:
+        take = order[done_rows:done_rows + max(1, cores)]
+        pj = np.repeat(take, W).astype(np.int32)
+        pi = np.tile(np.arange(W), len(take)).astype(np.int32)
+        t0 = time.perf_counter()
+        oracle.kde_pixels(g, cloud.x, cloud.y, pi, pj, threads=cores)
+        t_used += time.perf_counter() - t0
+        for j in take:
+            pairs += int(width[(rng_[:, 2] <= j) & (rng_[:, 3] >= j)].sum())
+        done_rows += len(take)
+    return {"value": pairs / t_used, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{done_rows} random full rows of {W} px over all {cfg['n']} points "
+                      f"({t_used:.1f} s, fp64 double loop)",
+            "seconds": round(t_used, 2)}
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return  # rank 0 alone runs the CPU oracle
+    cfg = CONFIGS[args.config]
+    cloud, x0, y0, res = _gen(cfg)
+    per = max(2.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
+    import oracle
+    oracle.build()
+    for _ in range(args.warmup):
+        cpu_baseline(cfg, cloud, x0, y0, res, seconds=per / 4)
+    vals = [cpu_baseline(cfg, cloud, x0, y0, res, seconds=per) for _ in range(args.steps)]
+    v = statistics.mean(x["value"] for x in vals)
+    W = cfg["W"]
+    ms = statistics.mean(x["seconds"] for x in vals) * 1e3
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (aisgen, seeded)",
+        "config": {"workload": WORKLOAD[args.config], "config": args.config,
+                   "n_points": cfg["n"], "grid": f"{W}x{W}", "h_px": cfg["hpx"],
+                   "cutoff": cfg["cutoff"], "kernel": cfg["kernel"], "parallelism": "host threads"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": vals[0]["cores"], "kind": "oracle",
+                         "sample": vals[0]["sample"]},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2", choices=list(CONFIGS))
+    ap.add_argument("--path", default="auto", choices=["auto", "direct", "tensor"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

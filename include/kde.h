@@ -1,0 +1,180 @@
+/*
+ * kde.h -- C ABI of libkde.so, the B200 (sm_100a) gridded kernel density
+ * estimate of arxiv 2004.13653's visualisation hot path.
+ *
+ * Citations: P:n = PAPER.md line n (the paper's LaTeX source).
+ * §2 restates the operation; DESIGN.md §5 lists the readings (R1..R17).
+ *
+ * What it computes (the north star's formula with the paper's Table 1
+ * kernels, and Eq. 7's truncated window):
+ *
+ *   density(i,j) = 1/(n * h_px^2) * sum_{p : S(i,j,p)} K(s,t),
+ *   s = (i + 1/2 - u_p)/h_px,  t = (j + 1/2 - v_p)/h_px,
+ *   u_p = (x_p - x0)/res,  v_p = (y_p - y0)/res,  h_px = h/res,
+ *   S: ceil(u_p - 1/2 - R) <= i <= floor(u_p - 1/2 + R), same for j,
+ *      with R = c_eff * h_px, c_eff = min(cutoff,1) for the compact kernels,
+ *      cutoff for the Gaussian (Eq. 8 P:175-181 inclusive "<=");
+ *   K(s,t) = k(s) k(t)            (product form, Table 1 as printed; default)
+ *   K(s,t) = c2 * khat(sqrt(s^2+t^2)) and s^2+t^2 <= c_eff^2   (KDE_RADIAL)
+ *
+ * Pixel (i,j) has centre (x0 + (i+1/2) res, y0 + (j+1/2) res); row j = 0 is
+ * the smallest y (Eq. 6's y~ = 1 at y_min).  Output is fp32,
+ * row-major out[(j - row_begin) * width + i].  n is the number of finite
+ * points passed to kde_load_points (points outside the raster stay in n).
+ * n = 0 gives an all-zero raster.
+ *
+ * Support decisions (S) are made once per point in IEEE fp64 (round to
+ * nearest, no contraction) during kde_load_points and carried as integer
+ * ranges, so the fp32 (DIRECT) and fp16-operand tensor-core (TENSOR)
+ * evaluations never disagree with the fp64 oracle about which box pairs are
+ * included.  The radial disk test is made per pair in fp32.
+ *
+ * Threading: one context per host thread; no global state except the
+ * thread-local error message.  No CPU fallback exists: every entry point
+ * that computes runs CUDA kernels on params.device.
+ */
+#ifndef KDE_H
+#define KDE_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define KDE_API __attribute__((visibility("default")))
+#else
+#define KDE_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Kernel ids in Table 1 order. */
+enum {
+    KDE_UNIFORM = 0,
+    KDE_TRIANGULAR = 1,
+    KDE_EPANECHNIKOV = 2,
+    KDE_QUARTIC = 3,
+    KDE_TRIWEIGHT = 4,
+    KDE_TRICUBE = 5,
+    KDE_GAUSSIAN = 6,
+    KDE_COSINE = 7
+};
+/* OR into kernel: radial form K = c2 * khat(||(s,t)||) (R1). */
+#define KDE_RADIAL 0x100
+
+/* Evaluation paths (kde_eval). */
+enum {
+    KDE_PATH_DIRECT = 0, /* fp32 FMA/MUFU tiled evaluation, all kernels, both forms   */
+    KDE_PATH_TENSOR = 1  /* tcgen05 tensor-core A*B^T, product form only (fp16 operands,
+                            10-bit mantissa like tf32, fp32 accumulation in TMEM)      */
+};
+
+/* Return codes. */
+enum {
+    KDE_OK = 0,
+    KDE_EINVAL = -1,        /* bad argument (see each call)                        */
+    KDE_ENOMEM = -2,        /* device allocation failed                            */
+    KDE_ECUDA = -3,         /* CUDA launch / runtime error (incl. earlier async)    */
+    KDE_EUNSUPPORTED = -4,  /* valid request this build does not implement         */
+    KDE_ESTATE = -5         /* call out of order (e.g. eval before load)           */
+};
+
+typedef struct kde_ctx kde_ctx; /* opaque; owns every device buffer it allocates */
+
+typedef struct {
+    double x0, y0;      /* raster lower-left corner, world units (e.g. Mercator metres)  */
+    double res;         /* pixel edge, world units; > 0 and finite                        */
+    int32_t width;      /* W columns (x), 1..32767                                        */
+    int32_t height;     /* H rows (y), 1..32767                                           */
+    double h;           /* bandwidth, world units; > 0 and finite                         */
+    int32_t kernel;     /* KDE_UNIFORM..KDE_COSINE, optionally | KDE_RADIAL               */
+    double cutoff;      /* support half-width in units of h; > 0 (compact kernels clamp
+                           it to 1); e.g. 4 for the Gaussian                               */
+    int32_t row_begin;  /* owned band [row_begin, row_end) for row-band sharding;          */
+    int32_t row_end;    /*   0,0 = all rows.  Otherwise 0 <= row_begin < row_end <= H.     */
+    int32_t device;     /* CUDA device ordinal                                            */
+} kde_params;
+
+typedef struct {
+    int64_t n_in;          /* points passed to the last kde_load_points                    */
+    int64_t n_finite;      /* finite points = the n of 1/(n h^2)                           */
+    int64_t n_binned;      /* points kept for evaluation                                   */
+    int64_t n_outside;     /* finite points dropped: window misses the raster, or (banded)
+                              home bucket row outside the band's reach                     */
+    int64_t useful_pairs;  /* sum over kept points of |box window clipped to raster
+                              columns x band rows| = (pixel, point) pairs inside the box
+                              support; the "kernel evaluations" of the metric              */
+    int32_t bucket;        /* bucket edge B in pixels (power of two)                       */
+    int32_t nbx, nby;      /* bucket grid ceil(W/B) x ceil(H/B)                            */
+    int32_t reach_px;      /* ceil(R + 1/2) + 1: max pixel distance window <- home pixel   */
+    int64_t kernel_launches; /* CUDA kernels this context has launched so far (cumulative)  */
+} kde_stats;
+
+/*
+ * kde_create: validate params, plan (bucket size, tiles), and bind the device.
+ * Allocates no point-sized buffers and launches no kernels.
+ *   p    [in]  parameters, copied.
+ *   out  [out] new context; set to NULL on error.
+ * Errors: KDE_EINVAL for NULL pointers, res/h/cutoff not > 0 or not finite,
+ *   width/height outside 1..32767, unknown kernel id or flag bits, band not
+ *   0,0 and not 0 <= row_begin < row_end <= height; KDE_ECUDA if the device
+ *   cannot be selected.
+ */
+KDE_API int kde_create(const kde_params* p, kde_ctx** out);
+
+/*
+ * kde_load_points: replace the context's point set and bin it (steps a1/a2).
+ *   x, y [in] n fp64 coordinates (world units), structure-of-arrays; either
+ *             both host pointers (copied to the device through a pinned staging
+ *             buffer) or both device pointers on params.device.  Not retained.
+ *   n    [in] >= 0 (0 is legal: kde_eval then writes zeros).
+ * Runs a1 (fp64 convert, integer support ranges, bucket keys), a2 (stable LSD
+ * counting sort by bucket key, gather to bucket-local fp32 SoA) and the
+ * evaluation plan on the context's internal stream, then synchronises it
+ * (the plan reads back the bucket offsets).  Non-finite points are dropped
+ * and not counted in n.
+ * Errors: KDE_EINVAL (NULL ctx, n < 0, NULL x/y with n > 0, mixed host/device),
+ *   KDE_ENOMEM, KDE_ECUDA.
+ */
+KDE_API int kde_load_points(kde_ctx* c, const double* x, const double* y, int64_t n);
+
+/*
+ * kde_eval: evaluate the band's raster (steps a3/a4 + a5) into out.
+ *   path   [in] KDE_PATH_DIRECT or KDE_PATH_TENSOR.
+ *   out    [out] device pointer on params.device, (row_end-row_begin)*width fp32
+ *                (all H*W when the band is 0,0), caller-owned; fully overwritten.
+ *   stream [in] cudaStream_t (NULL = legacy default stream).  Stream-ordered and
+ *               asynchronous: results are ready when the stream reaches this point.
+ * Deterministic: the same inputs give bitwise-identical output, and a banded
+ * context gives exactly the rows of the unbanded raster.
+ * Errors: KDE_EINVAL (NULL ctx/out, unknown path), KDE_ESTATE (no kde_load_points
+ *   yet), KDE_EUNSUPPORTED (TENSOR with a radial kernel), KDE_ECUDA (launch error,
+ *   or an earlier asynchronous fault).
+ */
+KDE_API int kde_eval(kde_ctx* c, int32_t path, float* out, void* stream);
+
+/* kde_get_stats: counters of the last load (all zero before one). EINVAL on NULL. */
+KDE_API int kde_get_stats(const kde_ctx* c, kde_stats* s);
+
+/*
+ * kde_get_bins: copy the binning result of the last load to HOST memory for
+ * inspection (bit-exact parity tests).  Any pointer may be NULL to skip it.
+ *   offsets [nbx*nby+1] int64   bucket start positions (exclusive scan of counts)
+ *   perm    [n_binned]  int64   original index of each sorted point
+ *   lx, ly  [n_binned]  float   bucket-local coordinates u - bx*B, v - by*B (fp64->RN fp32)
+ *   ranges  [4*n_binned] int32  i_lo, i_hi, j_lo, j_hi (clipped to the raster)
+ * Synchronous.  Errors: KDE_EINVAL, KDE_ESTATE, KDE_ECUDA.
+ */
+KDE_API int kde_get_bins(const kde_ctx* c, int64_t* offsets, int64_t* perm, float* lx, float* ly,
+                 int32_t* ranges);
+
+/* Thread-local message describing the last non-OK return on this thread. */
+KDE_API const char* kde_last_error(void);
+
+/* Release the context and every device buffer it owns. NULL-safe. */
+KDE_API void kde_free(kde_ctx* c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KDE_H */

@@ -1,0 +1,154 @@
+"""Thin ctypes binding of libkde.so (include/kde.h) -- argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels; this module only
+converts torch tensors / numpy arrays to pointers and return codes to
+exceptions.  There is no CPU fallback: if libkde.so is missing or cannot be
+loaded, importing the package raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libkde.so")
+
+KDE_UNIFORM, KDE_TRIANGULAR, KDE_EPANECHNIKOV, KDE_QUARTIC = 0, 1, 2, 3
+KDE_TRIWEIGHT, KDE_TRICUBE, KDE_GAUSSIAN, KDE_COSINE = 4, 5, 6, 7
+KDE_RADIAL = 0x100
+KERNEL_NAMES = ["uniform", "triangular", "epanechnikov", "quartic", "triweight", "tricube",
+                "gaussian", "cosine"]
+KDE_PATH_DIRECT, KDE_PATH_TENSOR = 0, 1
+KDE_OK, KDE_EINVAL, KDE_ENOMEM, KDE_ECUDA, KDE_EUNSUPPORTED, KDE_ESTATE = 0, -1, -2, -3, -4, -5
+_CODES = {KDE_EINVAL: "EINVAL", KDE_ENOMEM: "ENOMEM", KDE_ECUDA: "ECUDA",
+          KDE_EUNSUPPORTED: "EUNSUPPORTED", KDE_ESTATE: "ESTATE"}
+
+EXPORTS = ("kde_create", "kde_load_points", "kde_eval", "kde_get_stats", "kde_get_bins",
+           "kde_last_error", "kde_free")
+
+
+class kde_params(ctypes.Structure):
+    _fields_ = [("x0", ctypes.c_double), ("y0", ctypes.c_double), ("res", ctypes.c_double),
+                ("width", ctypes.c_int32), ("height", ctypes.c_int32), ("h", ctypes.c_double),
+                ("kernel", ctypes.c_int32), ("cutoff", ctypes.c_double),
+                ("row_begin", ctypes.c_int32), ("row_end", ctypes.c_int32),
+                ("device", ctypes.c_int32)]
+
+
+class kde_stats(ctypes.Structure):
+    _fields_ = [("n_in", ctypes.c_int64), ("n_finite", ctypes.c_int64),
+                ("n_binned", ctypes.c_int64), ("n_outside", ctypes.c_int64),
+                ("useful_pairs", ctypes.c_int64), ("bucket", ctypes.c_int32),
+                ("nbx", ctypes.c_int32), ("nby", ctypes.c_int32), ("reach_px", ctypes.c_int32),
+                ("kernel_launches", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {f: int(getattr(self, f)) for f, _ in self._fields_}
+
+
+class KdeError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{_CODES.get(code, code)}: {msg}")
+        self.code = code
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with "
+                          "`python -m paper_2004_13653_b200.build` (no CPU fallback exists)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp = ctypes.c_void_p
+    P = ctypes.POINTER
+    L.kde_create.argtypes = [P(kde_params), P(vp)]
+    L.kde_load_points.argtypes = [vp, vp, vp, ctypes.c_int64]
+    L.kde_eval.argtypes = [vp, ctypes.c_int32, vp, vp]
+    L.kde_get_stats.argtypes = [vp, P(kde_stats)]
+    L.kde_get_bins.argtypes = [vp, vp, vp, vp, vp, vp]
+    L.kde_last_error.restype = ctypes.c_char_p
+    L.kde_last_error.argtypes = []
+    L.kde_free.argtypes = [vp]
+    L.kde_free.restype = None
+    for f in ("kde_create", "kde_load_points", "kde_eval", "kde_get_stats", "kde_get_bins"):
+        getattr(L, f).restype = ctypes.c_int
+    return L
+
+
+_L = _load()
+
+
+def _check(rc):
+    if rc != KDE_OK:
+        raise KdeError(rc, _L.kde_last_error().decode(errors="replace"))
+
+
+def kde_last_error() -> str:
+    return _L.kde_last_error().decode(errors="replace")
+
+
+def _ptr(a):
+    """(pointer, device?) of a contiguous torch tensor or numpy array."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return a.ctypes.data
+    if not a.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return a.data_ptr()
+
+
+def kde_create(params: kde_params) -> int:
+    h = ctypes.c_void_p()
+    _check(_L.kde_create(ctypes.byref(params), ctypes.byref(h)))
+    return h.value
+
+
+def kde_load_points(ctx: int, x, y) -> None:
+    """x, y: float64 torch tensors (host or on the context's device) or numpy arrays."""
+    n = int(x.shape[0])
+    if int(y.shape[0]) != n:
+        raise ValueError("x and y lengths differ")
+    for a in (x, y):
+        dt = a.dtype
+        if (isinstance(a, np.ndarray) and dt != np.float64) or (not isinstance(a, np.ndarray)
+                                                                and str(dt) != "torch.float64"):
+            raise TypeError("coordinates must be float64")
+    _check(_L.kde_load_points(ctx, _ptr(x) if n else None, _ptr(y) if n else None, n))
+
+
+def kde_eval(ctx: int, path: int, out, stream: int | None = None) -> None:
+    """out: float32 CUDA tensor of band_rows*W; stream: raw cudaStream_t handle."""
+    if str(out.dtype) != "torch.float32" or not out.is_cuda:
+        raise TypeError("out must be a float32 CUDA tensor")
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream(out.device).cuda_stream
+    _check(_L.kde_eval(ctx, int(path), _ptr(out), stream))
+
+
+def kde_get_stats(ctx: int) -> dict:
+    s = kde_stats()
+    _check(_L.kde_get_stats(ctx, ctypes.byref(s)))
+    return s.as_dict()
+
+
+def kde_get_bins(ctx: int) -> dict:
+    st = kde_get_stats(ctx)
+    nb = st["nbx"] * st["nby"]
+    m = st["n_binned"]
+    off = np.zeros(nb + 1, np.int64)
+    perm = np.zeros(max(m, 1), np.int64)
+    lx = np.zeros(max(m, 1), np.float32)
+    ly = np.zeros(max(m, 1), np.float32)
+    rng = np.zeros((max(m, 1), 4), np.int32)
+    _check(_L.kde_get_bins(ctx, off.ctypes.data, perm.ctypes.data, lx.ctypes.data,
+                           ly.ctypes.data, rng.ctypes.data))
+    return dict(offsets=off, perm=perm[:m], lx=lx[:m], ly=ly[:m], ranges=rng[:m], stats=st)
+
+
+def kde_free(ctx: int | None) -> None:
+    if ctx:
+        _L.kde_free(ctx)

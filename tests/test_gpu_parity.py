@@ -1,0 +1,177 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle.
+
+Bars (BASELINE.json north_star):
+  * binning, indices, stats: bit-exact;
+  * direct fp32 path: max |gpu - oracle| <= 1e-5 * max(oracle) over the evaluated set;
+  * tensor-core path: <= 2e-3 * max(oracle).
+Radial parity excludes pixels the oracle flags as fp32 near-ties of the disk
+test (R3).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from tests.gpu_cases import (CONFIGS, THREADS, adversarial, case, hottest_bucket_tile,
+                             sample_pixels)
+
+pytestmark = pytest.mark.gpu
+
+TOL_DIRECT = 1e-5
+TOL_TENSOR = 2e-3
+
+
+def _kde(c, kernel=None, rows=None, cutoff=None):
+    from paper_2004_13653_b200 import KDE
+    k = c.get("kernel", 6) if kernel is None else kernel
+    cut = c.get("cutoff", 4.0) if cutoff is None else cutoff
+    return KDE(c["x0"], c["y0"], c["res"], c["W"], c["H"], c["h"], kernel=k, cutoff=cut, rows=rows)
+
+
+def _grid(c, kernel=None, rows=None, cutoff=None):
+    rb, re = (0, 0) if rows is None else rows
+    return oracle.Grid(c["x0"], c["y0"], c["res"], c["W"], c["H"], c["h"],
+                       c.get("kernel", 6) if kernel is None else kernel,
+                       c.get("cutoff", 4.0) if cutoff is None else cutoff, rb, re)
+
+
+def _err(gpu, ref, ties=None):
+    d = np.abs(gpu.astype(np.float64) - ref)
+    if ties is not None:
+        d = np.where(ties.astype(bool), 0.0, d)
+    return d.max() / max(ref.max(), 1e-300)
+
+
+# --- binning: bit-exact ------------------------------------------------------------
+BIN_CASES = {
+    "C1": lambda: case("estuary", 10_000, 256, 2.0, seed=CONFIGS["C1"][6]),
+    "adversarial": lambda: adversarial(),
+    "islands_ragged": lambda: case("islands", 50_000, 300, 3.0, seed=4, H=170),
+    "big_h": lambda: case("promontory", 30_000, 512, 20.0, seed=5),
+}
+
+
+@pytest.mark.parametrize("name", list(BIN_CASES))
+@pytest.mark.parametrize("rows", [None, (64, 150)])
+def test_binning_bit_exact(name, rows):
+    c = BIN_CASES[name]()
+    if rows is not None and rows[1] > c["H"]:
+        rows = (rows[0], c["H"])
+    k = _kde(c, rows=rows)
+    k.load(torch.from_numpy(c["x"]).cuda(), torch.from_numpy(c["y"]).cuda())
+    got = k.bins()
+    want = oracle.bin_points(_grid(c, rows=rows), got["stats"]["bucket"], c["x"], c["y"])
+    for f in ("n_in", "n_finite", "n_binned", "n_outside", "useful_pairs"):
+        assert got["stats"][f] == want["stats"][f], f
+    np.testing.assert_array_equal(got["offsets"], want["offsets"])
+    np.testing.assert_array_equal(got["perm"], want["perm"])
+    np.testing.assert_array_equal(got["ranges"], want["ranges"])
+    np.testing.assert_array_equal(got["lx"].view(np.uint32), want["lx"].view(np.uint32))
+    np.testing.assert_array_equal(got["ly"].view(np.uint32), want["ly"].view(np.uint32))
+    assert got["stats"]["reach_px"] == oracle.reach_px(_grid(c))
+
+
+def test_binning_host_and_device_inputs_identical():
+    c = BIN_CASES["adversarial"]()
+    a = _kde(c).load(torch.from_numpy(c["x"]), torch.from_numpy(c["y"]))
+    b = _kde(c).load(torch.from_numpy(c["x"]).cuda(), torch.from_numpy(c["y"]).cuda())
+    ra, rb = a.eval().cpu().numpy(), b.eval().cpu().numpy()
+    np.testing.assert_array_equal(ra.view(np.uint32), rb.view(np.uint32))
+    assert a.stats() == b.stats()
+
+
+# --- direct path: full raster, all kernels x forms -----------------------------------
+@pytest.mark.parametrize("kernel", [k | f for f in (0, 0x100) for k in range(8)])
+def test_direct_C1_full_raster(kernel):
+    preset, n, W, hpx, _, cut, seed = CONFIGS["C1"]
+    c = case(preset, n, W, hpx, seed=seed)
+    k = _kde(c, kernel=kernel)
+    k.load(torch.from_numpy(c["x"]).cuda(), torch.from_numpy(c["y"]).cuda())
+    gpu = k.eval("direct").cpu().numpy()
+    ref, nf, ties = oracle.kde_raster(_grid(c, kernel=kernel), c["x"], c["y"], threads=THREADS,
+                                      want_ties=True)
+    assert nf == k.stats()["n_finite"]
+    assert _err(gpu, ref, ties if kernel & 0x100 else None) <= TOL_DIRECT
+
+
+@pytest.mark.parametrize("kernel", [0, 2, 5, 6, 7, 6 | 0x100, 1 | 0x100])
+@pytest.mark.parametrize("cutoff", [4.0, 0.6])
+def test_direct_adversarial_ragged(kernel, cutoff):
+    c = adversarial()
+    k = _kde(c, kernel=kernel, cutoff=cutoff)
+    k.load(torch.from_numpy(c["x"]).cuda(), torch.from_numpy(c["y"]).cuda())
+    gpu = k.eval("direct").cpu().numpy()
+    ref, _, ties = oracle.kde_raster(_grid(c, kernel=kernel, cutoff=cutoff), c["x"], c["y"],
+                                     threads=THREADS, want_ties=True)
+    assert _err(gpu, ref, ties if kernel & 0x100 else None) <= TOL_DIRECT
+
+
+def test_direct_hot_pixel_split_k():
+    """All points in (nearly) one pixel: m ~ 6e4 contributions per pixel, forces split-K."""
+    rng = np.random.default_rng(3)
+    n = 60_000
+    res = 10.0
+    c = dict(x=1e6 + (40.3 + rng.normal(0, 0.2, n)) * res, y=2e6 + (21.7 + rng.normal(0, 0.2, n)) * res,
+             x0=1e6, y0=2e6, res=res, W=90, H=50, h=3.0 * res, kernel=6, cutoff=4.0)
+    k = _kde(c)
+    k.load(torch.from_numpy(c["x"]).cuda(), torch.from_numpy(c["y"]).cuda())
+    gpu = k.eval("direct").cpu().numpy()
+    ref, _ = oracle.kde_raster(_grid(c), c["x"], c["y"], threads=THREADS)
+    assert _err(gpu, ref) <= TOL_DIRECT
+
+
+def test_direct_empty_and_all_nan():
+    c = adversarial()
+    k = _kde(c)
+    k.load(torch.zeros(0, dtype=torch.float64), torch.zeros(0, dtype=torch.float64))
+    assert not k.eval().any()
+    k.load(torch.full((10,), float("nan"), dtype=torch.float64), torch.zeros(10, dtype=torch.float64))
+    assert not k.eval().any()
+    assert k.stats()["n_finite"] == 0
+
+
+def test_direct_deterministic_and_band_sharding_bitwise():
+    c = case("estuary", 200_000, 512, 4.0, seed=21)
+    full = _kde(c).load(torch.from_numpy(c["x"]).cuda(), torch.from_numpy(c["y"]).cuda())
+    a = full.eval().cpu().numpy()
+    b = full.eval().cpu().numpy()
+    np.testing.assert_array_equal(a.view(np.uint32), b.view(np.uint32))
+    parts = []
+    bands = [(0, 64), (64, 200), (200, 448), (448, 512)]
+    for rb, re in bands:
+        kb = _kde(c, rows=(rb, re)).load(torch.from_numpy(c["x"]).cuda(), torch.from_numpy(c["y"]).cuda())
+        parts.append(kb.eval().cpu().numpy())
+        assert kb.stats()["n_finite"] == full.stats()["n_finite"]
+    cat = np.concatenate(parts, axis=0)
+    np.testing.assert_array_equal(cat.view(np.uint32), a.view(np.uint32))
+
+
+@pytest.mark.parametrize("cfg", ["C2"])
+@pytest.mark.parametrize("kernel", [6, 2])
+def test_direct_full_size_sampled(cfg, kernel):
+    """BASELINE config at full size, in the bench's launch configuration, on sampled pixels."""
+    preset, n, W, hpx, _, cut, seed = CONFIGS[cfg]
+    c = case(preset, n, W, hpx, seed=seed)
+    k = _kde(c, kernel=kernel)
+    k.load(torch.from_numpy(c["x"]).cuda(), torch.from_numpy(c["y"]).cuda())
+    gpu = k.eval("direct").cpu().numpy()
+    hx, hy = hottest_bucket_tile(c["x"], c["y"], c["x0"], c["y0"], c["res"], W, W)
+    tiles = [(hx, hy, 64, 64), (0, 0, 16, 16), (W - 16, W - 16, 16, 16)]
+    pi, pj = sample_pixels(W, W, (0, W), gpu=gpu, tiles=tiles, n_random=2048, seed=seed)
+    ref, _ = oracle.kde_pixels(_grid(c, kernel=kernel), c["x"], c["y"], pi, pj, threads=THREADS)
+    got = gpu[pj, pi]
+    assert np.abs(got - ref).max() <= TOL_DIRECT * ref.max()
+    assert ref.max() >= 0.5 * gpu.max()  # the sample contains the peak region
+
+
+def test_error_paths_on_device():
+    from paper_2004_13653_b200 import KdeError, _lib
+    c = adversarial()
+    k = _kde(c, kernel=6 | 0x100)
+    with pytest.raises(KdeError) as e:
+        k.eval()
+    assert e.value.code == _lib.KDE_ESTATE
+    k.load(torch.from_numpy(c["x"]), torch.from_numpy(c["y"]))
+    with pytest.raises(KdeError) as e:
+        k.eval("tensor")
+    assert e.value.code == _lib.KDE_EUNSUPPORTED
