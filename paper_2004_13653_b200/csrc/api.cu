@@ -3,6 +3,7 @@
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -39,92 +40,66 @@ struct DeviceGuard {
     }
 };
 
-template <class T>
-static int upload(T** dptr, int* cap, const std::vector<T>& v, cudaStream_t s) {
-    const int need = (int)v.size();
-    if (need > *cap) {
-        if (*dptr) cudaFree(*dptr);
-        *dptr = nullptr;
-        if (cudaMalloc(dptr, sizeof(T) * need) != cudaSuccess) {
-            cudaGetLastError();
-            set_error("cudaMalloc for plan failed");
-            return KDE_ENOMEM;
-        }
-        *cap = need;
+static int dalloc(void** p, size_t bytes, const char* what) {
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    if (cudaMalloc(p, bytes ? bytes : 16) != cudaSuccess) {
+        cudaGetLastError();
+        set_error("cudaMalloc for %s failed (%zu bytes)", what, bytes);
+        return KDE_ENOMEM;
     }
-    if (need) cudaMemcpyAsync(*dptr, v.data(), sizeof(T) * need, cudaMemcpyHostToDevice, s);
     return KDE_OK;
 }
 
-// Work plan for one evaluation path: tiles of tile_w x tile_h over the band, each with its
-// neighbourhood candidate count from the bucket offsets; tiles with more than `seg`
-// candidates are split into fixed-size segments (split-K).  Depends only on the
-// neighbourhood contents, so a banded context plans each tile exactly as the unbanded one.
-int build_plan(kde_ctx* c, int tile_w, int tile_h, int seg, EvalPlan& pl, int64_t slot_floats) {
-    const Geom& g = c->g;
-    pl.items.clear();
-    pl.reds.clear();
-    pl.nslots = 0;
-    pl.any_empty = false;
-    pl.ntx = (g.W + tile_w - 1) / tile_w;
-    pl.nty0 = g.rb / tile_h;
-    pl.nty1 = (g.re + tile_h - 1) / tile_h;
-    const std::vector<uint32_t>& off = c->h_offsets;
-    for (int ty = pl.nty0; ty < pl.nty1; ty++) {
-        const int Y0 = ty * tile_h;
-        const int by0 = std::max(Y0 / kBucket - g.nr, 0);
-        const int by1 = std::min((Y0 + tile_h - 1) / kBucket + g.nr, g.nby - 1);
-        for (int tx = 0; tx < pl.ntx; tx++) {
-            const int X0 = tx * tile_w;
-            const int bx0 = std::max(X0 / kBucket - g.nr, 0);
-            const int bx1 = std::min((X0 + tile_w - 1) / kBucket + g.nr, g.nbx - 1);
-            int64_t cand = 0;
-            for (int by = by0; by <= by1; by++)
-                cand += (int64_t)off[(size_t)by * g.nbx + bx1 + 1] - off[(size_t)by * g.nbx + bx0];
-            if (cand == 0) {
-                pl.any_empty = true;
-                continue;
-            }
-            const int nseg = (int)((cand + seg - 1) / seg);
-            if (nseg == 1) {
-                pl.items.push_back({tx, ty, 0, (int)cand, -1, 0});
-            } else {
-                const int slot0 = pl.nslots;
-                pl.nslots += nseg;
-                for (int k = 0; k < nseg; k++)
-                    pl.items.push_back({tx, ty, k * seg, (int)std::min<int64_t>(cand, (int64_t)(k + 1) * seg),
-                                        slot0 + k, 0});
-                pl.reds.push_back({tx, ty, slot0, nseg});
-            }
+// Splat-pass geometry, fixed at create: sub-windows of the group window B + 2F, and the
+// register micro-tile edge whose thread grid best fills whole warps.
+static void plan_geometry(EvalPlan& pl, const Geom& g) {
+    const int Wd = g.B + 2 * g.F;
+    pl.nsubx = (Wd + kSub - 1) / kSub;
+    pl.S = (Wd + pl.nsubx - 1) / pl.nsubx;  // equal sub-windows (the last may be smaller)
+    double best = -1.0;
+    for (int mt = 3; mt <= 6; mt++) {
+        const int nm = (pl.S + mt - 1) / mt;
+        if (nm * nm > 256) continue;
+        const int thr = ((nm * nm + 31) / 32) * 32;
+        const double cover = (double)pl.S / (nm * mt);
+        const double util = cover * cover * (double)(nm * nm) / thr + 1e-3 * mt;
+        if (util > best) {
+            best = util;
+            pl.mt = mt;
+            pl.threads = thr;
         }
     }
-    // heaviest first: the block scheduler then approximates longest-processing-time order
-    std::stable_sort(pl.items.begin(), pl.items.end(), [](const WorkItem& a, const WorkItem& b) {
-        return (a.k1 - a.k0) > (b.k1 - b.k0);
-    });
-    int rc = upload(&pl.d_items, &pl.d_items_cap, pl.items, c->stream);
-    if (rc) return rc;
-    rc = upload(&pl.d_reds, &pl.d_reds_cap, pl.reds, c->stream);
-    if (rc) return rc;
-    const int64_t need = (int64_t)pl.nslots * slot_floats;
-    if (need > pl.partial_cap) {
-        if (pl.d_partial) cudaFree(pl.d_partial);
-        pl.d_partial = nullptr;
-        if (cudaMalloc(&pl.d_partial, sizeof(float) * need) != cudaSuccess) {
-            cudaGetLastError();
-            set_error("cudaMalloc for split-K partials failed");
-            return KDE_ENOMEM;
-        }
-        pl.partial_cap = need;
-    }
-    return KDE_OK;
+    const int nm = (pl.S + pl.mt - 1) / pl.mt;
+    pl.slot_ld = nm * pl.mt;
+    pl.ld = nm * (pl.mt <= 4 ? 4 : 8) + 4;
 }
 
 static void free_plan(EvalPlan& pl) {
+    cudaFree(pl.d_full);
+    cudaFree(pl.d_part);
+    cudaFree(pl.d_nseg);
+    cudaFree(pl.d_scan_tmp);
+    cudaFree(pl.d_group);
+    cudaFree(pl.d_totals);
     cudaFree(pl.d_items);
-    cudaFree(pl.d_reds);
-    cudaFree(pl.d_partial);
+    cudaFree(pl.d_splat);
+    cudaFree(pl.d_done);
     pl = EvalPlan();
+}
+
+// Bucket (point-group) edge B: small enough that the group window B + 2F stays close to
+// the (2R+1) support, large enough that groups hold many points.
+static int choose_bucket(double R) {
+    const char* env = getenv("KDE_BUCKET");
+    if (env) {
+        const int b = atoi(env);
+        if (b == 4 || b == 8 || b == 16 || b == 32 || b == 64) return b;
+    }
+    if (R < 24.0) return 8;
+    if (R < 64.0) return 16;
+    if (R < 160.0) return 32;
+    return 64;
 }
 
 static bool is_device_ptr(const void* p, int* dev) {
@@ -195,8 +170,10 @@ int kde_create(const kde_params* p, kde_ctx** out) {
     g.H = p->height;
     g.rb = rb;
     g.re = re;
-    g.nbx = (g.W + kBucket - 1) / kBucket;
-    g.nby = (g.H + kBucket - 1) / kBucket;
+    g.B = choose_bucket(g.R);
+    g.F = (int)floor(g.R + 0.5);
+    g.nbx = (g.W + g.B - 1) / g.B;
+    g.nby = (g.H + g.B - 1) / g.B;
     const double reach = ceil(g.R + 0.5) + 1.0;
     if (!(reach < 1.0e6)) {
         delete c;
@@ -204,19 +181,39 @@ int kde_create(const kde_params* p, kde_ctx** out) {
         return KDE_EINVAL;
     }
     g.reach = (int)reach;
-    g.nr = (g.reach + kBucket - 1) / kBucket;
-    g.band_lo = rb / kBucket - g.nr;
-    g.band_hi = (re - 1) / kBucket + g.nr;
+    {   // combine-pass entry list bound: groups meeting a 32-px tile x <= 4 sub-windows
+        const int Wd = g.B + 2 * g.F;
+        const int per = (kCombTile + Wd) / g.B + 2;
+        if (per * per * 4 > 2048) {
+            delete c;
+            set_error("kde_create: support R = %g px too large for bucket %d", g.R, g.B);
+            return KDE_EINVAL;
+        }
+    }
+    g.nr = (g.reach + g.B - 1) / g.B;
+    g.band_lo = rb / g.B - g.nr;
+    g.band_hi = (re - 1) / g.B + g.nr;
     const size_t nb = (size_t)g.nbx * g.nby;
-    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    plan_geometry(c->plan, g);
+    // a BLOCKING stream: loads are ordered after work on the legacy default stream
+    // (where device-resident inputs are usually produced, e.g. by PyTorch's default stream)
+    cudaError_t e = cudaStreamCreate(&c->stream);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->loaded_ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaMallocHost(&c->h_totals, 64);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_offsets, sizeof(uint32_t) * (nb + 1));
     if (e == cudaSuccess) e = cudaMalloc(&c->d_stats, sizeof(unsigned long long) * 4);
+    EvalPlan& pl = c->plan;
+    if (e == cudaSuccess) e = cudaMalloc(&pl.d_full, sizeof(uint32_t) * (nb + 1));
+    if (e == cudaSuccess) e = cudaMalloc(&pl.d_part, sizeof(uint32_t) * (nb + 1));
+    if (e == cudaSuccess) e = cudaMalloc(&pl.d_nseg, sizeof(uint32_t) * (nb + 1));
+    if (e == cudaSuccess) e = cudaMalloc(&pl.d_scan_tmp, sizeof(uint32_t) * ((nb + 1) / 2048 + 2));
+    if (e == cudaSuccess) e = cudaMalloc(&pl.d_group, sizeof(int2) * nb);
+    if (e == cudaSuccess) e = cudaMalloc(&pl.d_totals, sizeof(int) * 4);
     if (e != cudaSuccess) {
         kde_free(c);
         return cuda_fail(e, "kde_create: allocation");
     }
-    c->h_offsets.assign(nb + 1, 0u);
-    c->stats.bucket = kBucket;
+    c->stats.bucket = g.B;
     c->stats.nbx = g.nbx;
     c->stats.nby = g.nby;
     c->stats.reach_px = g.reach;
@@ -274,26 +271,42 @@ int kde_load_points(kde_ctx* c, const double* x, const double* y, int64_t n) {
     }
     int rc = bin_points(c, dx, dy, n);
     if (rc) return rc;
-    const size_t nb = (size_t)c->g.nbx * c->g.nby;
-    unsigned long long st[3];
-    cudaMemcpyAsync(c->h_offsets.data(), c->d_offsets, sizeof(uint32_t) * (nb + 1),
+    rc = plan_device(c);
+    if (rc) return rc;
+    // one small readback: plan totals (TF, TP, nslots, n_binned) + integer stats
+    cudaMemcpyAsync(c->h_totals, c->plan.d_totals, 4 * sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+    cudaMemcpyAsync(c->h_totals + 4, c->d_stats, 3 * sizeof(unsigned long long),
                     cudaMemcpyDeviceToHost, c->stream);
-    cudaMemcpyAsync(st, c->d_stats, sizeof st, cudaMemcpyDeviceToHost, c->stream);
     cudaError_t e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) return cuda_fail(e, "kde_load_points");
+    const unsigned long long* st = reinterpret_cast<const unsigned long long*>(c->h_totals + 4);
     c->stats.n_in = n;
     c->stats.n_finite = (int64_t)st[0];
     c->stats.n_outside = (int64_t)st[1];
     c->stats.useful_pairs = (int64_t)st[2];
-    c->stats.n_binned = (int64_t)c->h_offsets[nb];
-    rc = build_plan(c, kDirTile, kDirTile, kSegCands, c->plan_dir, (int64_t)kDirTile * kDirTile);
-    if (rc) return rc;
-    if (c->kern == KDE_GAUSSIAN && !c->radial) {
-        rc = build_plan(c, kTcN, kTcM, kTcSegCands, c->plan_tc, (int64_t)kTcM * kTcN);
-        if (rc) return rc;
+    c->stats.n_binned = (int64_t)c->h_totals[3];
+    EvalPlan& pl = c->plan;
+    const int nsub = pl.nsubx * pl.nsubx;
+    pl.tf = c->h_totals[0];
+    pl.tp = c->h_totals[1];
+    pl.nslots = c->h_totals[2];
+    pl.nitems = (pl.tf + pl.tp) * nsub;
+    if (pl.nitems > pl.items_cap) {
+        if (dalloc((void**)&pl.d_items, sizeof(int4) * pl.nitems, "splat items")) return KDE_ENOMEM;
+        pl.items_cap = pl.nitems;
     }
-    e = cudaStreamSynchronize(c->stream);
-    if (e != cudaSuccess) return cuda_fail(e, "kde_load_points: plan upload");
+    if (pl.nslots > pl.slots_cap) {
+        if (dalloc((void**)&pl.d_splat, sizeof(float) * (size_t)pl.nslots * pl.slot_ld * pl.slot_ld,
+                   "splat blocks"))
+            return KDE_ENOMEM;
+        if (dalloc((void**)&pl.d_done, sizeof(int) * ((size_t)pl.nslots + 1), "splat counters"))
+            return KDE_ENOMEM;
+        pl.slots_cap = pl.nslots;
+    }
+    rc = plan_scatter(c);
+    if (rc) return rc;
+    e = cudaEventRecord(c->loaded_ev, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "kde_load_points: event");
     c->loaded = true;
     return KDE_OK;
 }
@@ -320,6 +333,8 @@ int kde_eval(kde_ctx* c, int32_t path, float* out, void* stream) {
     cudaError_t e = cudaGetLastError();  // surface earlier asynchronous faults
     if (e != cudaSuccess) return cuda_fail(e, "kde_eval: earlier asynchronous error");
     cudaStream_t s = (cudaStream_t)stream;
+    e = cudaStreamWaitEvent(s, c->loaded_ev, 0);  // the plan scatter of the last load
+    if (e != cudaSuccess) return cuda_fail(e, "kde_eval: wait for load");
     return path == KDE_PATH_DIRECT ? launch_direct(c, out, s) : launch_tc(c, out, s);
 }
 
@@ -346,8 +361,14 @@ int kde_get_bins(const kde_ctx* c, int64_t* offsets, int64_t* perm, float* lx, f
     DeviceGuard dg(c->p.device);
     const size_t nb = (size_t)c->g.nbx * c->g.nby;
     const size_t m = (size_t)c->stats.n_binned;
-    if (offsets)
-        for (size_t b = 0; b <= nb; b++) offsets[b] = (int64_t)c->h_offsets[b];
+    if (cudaEventSynchronize(c->loaded_ev) != cudaSuccess) return cuda_fail(cudaGetLastError(), "kde_get_bins");
+    if (offsets) {
+        std::vector<uint32_t> ov(nb + 1);
+        const cudaError_t e0 = cudaMemcpy(ov.data(), c->d_offsets, sizeof(uint32_t) * (nb + 1),
+                                          cudaMemcpyDeviceToHost);
+        if (e0 != cudaSuccess) return cuda_fail(e0, "kde_get_bins");
+        for (size_t b = 0; b <= nb; b++) offsets[b] = (int64_t)ov[b];
+    }
     if (m == 0) return KDE_OK;
     std::vector<uint32_t> pv;
     std::vector<float2> xy;
@@ -399,9 +420,10 @@ void kde_free(kde_ctx* c) {
     cudaFree(pb.rng);
     cudaFree(c->d_offsets);
     cudaFree(c->d_stats);
-    free_plan(c->plan_dir);
-    free_plan(c->plan_tc);
+    free_plan(c->plan);
     if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->loaded_ev) cudaEventDestroy(c->loaded_ev);
+    if (c->h_totals) cudaFreeHost(c->h_totals);
     delete c;
     if (prev >= 0) cudaSetDevice(prev);
 }

@@ -44,7 +44,7 @@ __device__ __forceinline__ Binned bin_point(double x, double y, const Geom& g, u
     const double fu = floor(u), fv = floor(v);
     const int hx = fu < 0.0 ? 0 : (fu > (double)(g.W - 1) ? g.W - 1 : (int)fu);
     const int hy = fv < 0.0 ? 0 : (fv > (double)(g.H - 1) ? g.H - 1 : (int)fv);
-    const int bx = hx / kBucket, by = hy / kBucket;
+    const int bx = hx / g.B, by = hy / g.B;
     if (by < g.band_lo || by > g.band_hi) return b;  // outside the band's reach
     b.status = 2;
     b.key = (uint32_t)(by * g.nbx + bx);
@@ -52,8 +52,8 @@ __device__ __forceinline__ Binned bin_point(double x, double y, const Geom& g, u
     b.ihi = (int)ihi;
     b.jlo = (int)jlo;
     b.jhi = (int)jhi;
-    b.lx = __double2float_rn(__dsub_rn(u, (double)(bx * kBucket)));
-    b.ly = __double2float_rn(__dsub_rn(v, (double)(by * kBucket)));
+    b.lx = __double2float_rn(__dsub_rn(u, (double)(bx * g.B)));
+    b.ly = __double2float_rn(__dsub_rn(v, (double)(by * g.B)));
     return b;
 }
 
@@ -289,7 +289,7 @@ static int grow(void** p, size_t bytes) {
     return KDE_OK;
 }
 
-static int scan_excl(uint32_t* a, int64_t L, uint32_t* tmp, cudaStream_t s) {
+int scan_excl_u32(uint32_t* a, int64_t L, uint32_t* tmp, cudaStream_t s) {
     if (L <= 0) return 0;
     const int nblk = (int)((L + kScanChunk - 1) / kScanChunk);
     scan_sums_kernel<<<nblk, 256, 0, s>>>(a, L, tmp);
@@ -336,7 +336,7 @@ int bin_points(kde_ctx* c, const double* d_x, const double* d_y, int64_t n64) {
         for (int ps = 0; ps < passes; ps++) {
             const int shift = ps * 8;
             rs_upsweep<<<nblk, kRsThreads, 0, s>>>(pb.key[cur], n, shift, pb.hist, nblk);
-            c->launches += 2 + scan_excl(pb.hist, (int64_t)256 * nblk, pb.scan_tmp, s);
+            c->launches += 2 + scan_excl_u32(pb.hist, (int64_t)256 * nblk, pb.scan_tmp, s);
             rs_downsweep<<<nblk, kRsThreads, 0, s>>>(pb.key[cur], ps == 0 ? nullptr : pb.val[cur],
                                                      pb.key[cur ^ 1], pb.val[cur ^ 1], n, shift,
                                                      pb.hist, nblk);

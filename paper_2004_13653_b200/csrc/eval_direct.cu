@@ -1,277 +1,389 @@
-// Step a3 (+ fused a5): direct tiled evaluation for all 8 Table-1 kernels, product or
-// radial form, fp32.
+// Step a3 (+ fused a5): direct fp32 evaluation for all 8 Table-1 kernels, product or
+// radial form.
 //
 // Prior art: the paper's §IV-B-2 convolution tiles the output in a thread
-// grid, stages the input tile + halo in shared memory, keeps the kernel in constant
-// memory and unrolls for ILP.  Here the input is the continuous point set, so per
-// 64x64 output tile one CTA:
-//   1. streams the tile's neighbourhood buckets (contiguous ranges of the sorted SoA,
-//      coalesced), culls points whose integer box misses the tile and compacts the
-//      survivors IN ORDER into shared memory (ballot + warp prefix);
-//   2. per chunk of 64 survivors, evaluates the 1-D factors khat(s) for the tile's 64
-//      columns and khat(t) for its 64 rows once per CTA into shared memory (masked by
-//      the fp64-decided integer ranges);
-//   3. each warp owns a 32x16 sub-tile, skips points whose box misses it (warp-uniform
-//      ballot masks), and each lane accumulates a 4x4 register micro-tile with one FFMA
-//      per (pixel, point) pair: acc += ky[r] * kx[c];
-//   4. blocked fp32 accumulation: per-chunk partials are added into running totals
-//      (R10), and the epilogue multiplies by C/(n h_px^2) (step a5).
-// Heavy tiles are split along the candidate list into fixed-size segments (split-K);
-// segment partials are summed in segment order by reduce_kernel -> deterministic.
+// grid, stages input tile + halo in shared memory, keeps the kernel in constant memory
+// and unrolls for ILP.  On B200 with continuous point coordinates the cost that matters
+// is geometric waste: a SIMT lane owns fixed pixels, so a point's (2R+1)^2 window must be
+// computed over every register tile it touches.  AIS points are concentrated (lanes,
+// anchorages: >90% of points share an 8x8-pixel home bucket with >=128 others), so the
+// register tiles are aligned to the POINT GROUPS instead of the output grid:
+//
+//   splat pass   one CTA per (bucket g, segment of <= 1024 of its points, 64x64 sub-window
+//                of g's window [bx*B - F, bx*B + B - 1 + F]^2, F = floor(R + 1/2)).  Per
+//                chunk of 32 points the CTA evaluates the 1-D factors khat(s) for the
+//                window's columns and khat(t) for its rows once into shared memory
+//                (masked by the fp64-decided integer ranges; double-buffered, one barrier
+//                per chunk), and each thread accumulates a 4x4 register micro-tile with one
+//                FFMA per (pixel, point) pair: acc += ky[r] * kx[c].  Blocked fp32
+//                accumulation (per-chunk partials into running totals, R10).
+//                The block is written to its splat slot.
+//   combine pass one CTA per 32x32 output tile sums, for every pixel, the splat blocks of
+//                the groups whose window covers it, in a fixed order (group row-major, then
+//                segment), and multiplies by C/(n h_px^2) (step a5).  Deterministic; a band
+//                computes exactly the same splats, so sharded == unsharded bitwise.
 #include "internal.cuh"
 #include "kernels.cuh"
 
 namespace kde {
 
-struct DirectArgs {
+struct SplatArgs {
     Geom g;
     const uint32_t* __restrict__ offsets;
     const float2* __restrict__ xy;
     const uint2* __restrict__ rng;
-    const WorkItem* __restrict__ items;
-    float* __restrict__ out;
-    float* __restrict__ partial;
+    const int4* __restrict__ items;   // (bucket, k0, k1, slot)
+    const int2* __restrict__ group;   // per bucket: (slot of segment 0, #segments)
+    int* __restrict__ done;           // per slot arrival counters; done[nslots] = work queue
+    float* __restrict__ splat;
+    int nitems, nslots, nsubx, S;
     KConst k;
     float c2;     // radial: c_eff^2
-    float scale;  // C / (n h_px^2)
+    float q2;     // Gaussian recurrence step 2^(2 kq)
+    bool recur;   // recurrence safe: 2^(kq (R + 8)^2) stays a normal float
+    int ld;       // factor row stride (floats)
+    int slot_ld;  // splat slot edge (floats): ceil(S/MT)*MT
 };
 
-constexpr int kT = kDirTile;     // 64
-constexpr int kCh = 64;          // points per factor chunk
-constexpr int kLd = kT + 4;      // padded factor row (floats)
-constexpr int kStage = 256;      // candidates examined per staging step
-constexpr int kMaxRowB = 64;     // max buckets per neighbourhood row held in smem
+constexpr int kChunk = 32;         // points per factor chunk (one per lane)
 
-template <int KERN, bool RADIAL>
-__global__ void __launch_bounds__(256, 2) direct_kernel(const DirectArgs a) {
-    __shared__ __align__(16) float s_fx[kCh][kLd];
-    __shared__ __align__(16) float s_fy[kCh][kLd];
-    __shared__ float2 s_cxy[kCh + kStage];
-    __shared__ int4 s_crng[kCh + kStage];
-    __shared__ uint32_t s_rowb[kMaxRowB + 1];
-    __shared__ int s_wsum[8];
+__device__ __forceinline__ int floor_div(int a, int b) {
+    return a >= 0 ? a / b : -((-a + b - 1) / b);
+}
 
-    const Geom& g = a.g;
-    const WorkItem w = a.items[blockIdx.x];
-    const int X0 = w.tx * kT, Y0 = w.ty * kT;
-    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-    const int wx = warp & 1, wy = warp >> 1;     // warp sub-tile 32 cols x 16 rows
-    const int lx = lane & 7, ly = lane >> 3;     // lane micro-tile 4 cols x 4 rows
-    const int c0 = wx * 32 + lx * 4, r0 = wy * 16 + ly * 4;
-    const uint32_t lt_mask = (1u << lane) - 1u;
+// factor-row stride per micro-tile column group (floats): keeps vector loads aligned
+template <int MT>
+constexpr int mt_stride() { return MT <= 4 ? 4 : 8; }
 
-    const int bx0 = max(X0 / kBucket - g.nr, 0);
-    const int bx1 = min((X0 + kT - 1) / kBucket + g.nr, g.nbx - 1);
-    const int by0 = max(Y0 / kBucket - g.nr, 0);
-    const int by1 = min((Y0 + kT - 1) / kBucket + g.nr, g.nby - 1);
-    const int nbr = bx1 - bx0 + 1;
-
-    float acc[4][4], tot[4][4];
-#pragma unroll
-    for (int r = 0; r < 4; r++)
-#pragma unroll
-        for (int c = 0; c < 4; c++) acc[r][c] = tot[r][c] = 0.f;
-
-    // --- one chunk of m <= 64 compacted points at s_cxy/s_crng[base..base+m) ---------
-    auto process_chunk = [&](int base, int m) {
-        {  // factors: thread -> point p = t/4, 16 columns and 16 rows
-            const int p = t >> 2, q = (t & 3) * 16;
-            if (p < m) {
-                const float2 P = s_cxy[base + p];
-                const int4 rr = s_crng[base + p];
-#pragma unroll
-                for (int k = 0; k < 16; k += 4) {
-                    float4 fx, fy;
-                    float* px = &fx.x;
-                    float* py = &fy.x;
-#pragma unroll
-                    for (int e = 0; e < 4; e++) {
-                        const int c = q + k + e;
-                        const float dx = ((float)c + 0.5f) - P.x;
-                        const float dy = ((float)c + 0.5f) - P.y;
-                        const bool inx = (unsigned)(c - rr.x) <= (unsigned)(rr.y - rr.x);
-                        const bool iny = (unsigned)(c - rr.z) <= (unsigned)(rr.w - rr.z);
-                        if constexpr (RADIAL) {
-                            px[e] = inx ? dx * dx * a.k.inv_h2 : __int_as_float(0x7f800000);
-                            py[e] = iny ? dy * dy * a.k.inv_h2 : __int_as_float(0x7f800000);
-                        } else {
-                            px[e] = inx ? khat<KERN>(dx, a.k) : 0.f;
-                            py[e] = iny ? khat<KERN>(dy, a.k) : 0.f;
-                        }
-                    }
-                    *reinterpret_cast<float4*>(&s_fx[p][q + k]) = fx;
-                    *reinterpret_cast<float4*>(&s_fy[p][q + k]) = fy;
-                }
-            }
-        }
-        // warp culling masks: which of the chunk's points touch this warp's sub-tile
-        uint32_t mk[2];
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-            const int p = lane + 32 * h;
-            bool hit = false;
-            if (p < m) {
-                const int4 rr = s_crng[base + p];
-                hit = rr.x <= wx * 32 + 31 && rr.y >= wx * 32 && rr.z <= wy * 16 + 15 &&
-                      rr.w >= wy * 16;
-            }
-            mk[h] = __ballot_sync(0xffffffffu, hit);
-        }
-        __syncthreads();
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-            uint32_t msk = mk[h];
-            while (msk) {
-                const int p = __ffs(msk) - 1 + 32 * h;
-                msk &= msk - 1;
-                const float4 fx = *reinterpret_cast<const float4*>(&s_fx[p][c0]);
-                const float4 fy = *reinterpret_cast<const float4*>(&s_fy[p][r0]);
-                const float vx[4] = {fx.x, fx.y, fx.z, fx.w};
-                const float vy[4] = {fy.x, fy.y, fy.z, fy.w};
-#pragma unroll
-                for (int r = 0; r < 4; r++)
-#pragma unroll
-                    for (int c = 0; c < 4; c++) {
-                        if constexpr (RADIAL) {
-                            const float r2 = vx[c] + vy[r];
-                            acc[r][c] += (r2 <= a.c2) ? khat_r<KERN>(r2) : 0.f;
-                        } else {
-                            acc[r][c] = fmaf(vy[r], vx[c], acc[r][c]);
-                        }
-                    }
-            }
-        }
-#pragma unroll
-        for (int r = 0; r < 4; r++)
-#pragma unroll
-            for (int c = 0; c < 4; c++) {
-                tot[r][c] += acc[r][c];
-                acc[r][c] = 0.f;
-            }
-        __syncthreads();
-    };
-
-    int cnt = 0;  // compacted points waiting in s_cxy/s_crng
-    int pos = 0;  // candidate position of the current row's first point
-    for (int by = by0; by <= by1; by++) {
-        const uint32_t* orow = a.offsets + (size_t)by * g.nbx;
-        const int rlo = (int)orow[bx0], rhi = (int)orow[bx1 + 1];
-        const int len = rhi - rlo;
-        const int lo = max(w.k0 - pos, 0), hi = min(w.k1 - pos, len);
-        pos += len;
-        if (lo >= hi) continue;
-        __syncthreads();
-        if (t <= nbr && t <= kMaxRowB) s_rowb[t] = orow[bx0 + t];
-        __syncthreads();
-        for (int sb = lo; sb < hi; sb += kStage) {
-            const int i = sb + t;
-            bool keep = false;
-            float2 P = make_float2(0.f, 0.f);
-            int4 rr = make_int4(0, 0, 0, 0);
-            if (i < hi) {
-                const uint32_t d = (uint32_t)(rlo + i);
-                const uint2 q = a.rng[d];
-                rr = make_int4((int)(q.x & 0xffffu) - X0, (int)(q.x >> 16) - X0,
-                               (int)(q.y & 0xffffu) - Y0, (int)(q.y >> 16) - Y0);
-                keep = rr.x <= kT - 1 && rr.y >= 0 && rr.z <= kT - 1 && rr.w >= 0;
-                if (keep) {
-                    int bx = bx0;
-                    if (nbr <= kMaxRowB) {
-                        for (int b = 1; b < nbr; b++) bx += (d >= s_rowb[b]);
-                    } else {
-                        for (int b = 1; b < nbr; b++) bx += (d >= orow[bx0 + b]);
-                    }
-                    const float2 l = a.xy[d];
-                    P = make_float2(l.x + (float)(bx * kBucket - X0), l.y + (float)(by * kBucket - Y0));
-                }
-            }
-            const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-            if (lane == 0) s_wsum[warp] = __popc(bal);
-            __syncthreads();
-            int wpre = 0, add = 0;
-#pragma unroll
-            for (int k = 0; k < 8; k++) {
-                const int v = s_wsum[k];
-                wpre += (k < warp) ? v : 0;
-                add += v;
-            }
-            if (keep) {
-                const int slot = cnt + wpre + __popc(bal & lt_mask);
-                s_cxy[slot] = P;
-                s_crng[slot] = rr;
-            }
-            __syncthreads();
-            cnt += add;
-            int done = 0;
-            while (cnt - done >= kCh) {
-                process_chunk(done, kCh);
-                done += kCh;
-            }
-            if (done > 0) {  // move the (< 64) leftovers to the front, order kept
-                const int rem = cnt - done;
-                float2 tp = make_float2(0.f, 0.f);
-                int4 tr = make_int4(0, 0, 0, 0);
-                if (t < rem) {
-                    tp = s_cxy[done + t];
-                    tr = s_crng[done + t];
-                }
-                __syncthreads();
-                if (t < rem) {
-                    s_cxy[t] = tp;
-                    s_crng[t] = tr;
-                }
-                __syncthreads();
-                cnt = rem;
-            }
-        }
-    }
-    if (cnt > 0) process_chunk(0, cnt);
-
-    // epilogue (a5): scale + store own band rows, or write the raw partial
-    if (w.slot < 0) {
-#pragma unroll
-        for (int r = 0; r < 4; r++) {
-            const int gy = Y0 + r0 + r;
-            if (gy < g.rb || gy >= g.re) continue;
-            float* orow = a.out + (size_t)(gy - g.rb) * g.W;
-#pragma unroll
-            for (int c = 0; c < 4; c++) {
-                const int gx = X0 + c0 + c;
-                if (gx < g.W) orow[gx] = tot[r][c] * a.scale;
-            }
-        }
+template <int MT>
+__device__ __forceinline__ void lds_mt(const float* p, float (&v)[MT]) {
+    if constexpr (MT == 3) {
+        const float2 a = *reinterpret_cast<const float2*>(p);
+        v[0] = a.x; v[1] = a.y; v[2] = p[2];
+    } else if constexpr (MT == 4) {
+        const float4 a = *reinterpret_cast<const float4*>(p);
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    } else if constexpr (MT == 5) {
+        const float4 a = *reinterpret_cast<const float4*>(p);
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = p[4];
     } else {
-        float* pp = a.partial + (size_t)w.slot * kT * kT;
-#pragma unroll
-        for (int r = 0; r < 4; r++)
-            *reinterpret_cast<float4*>(&pp[(r0 + r) * kT + c0]) =
-                make_float4(tot[r][0], tot[r][1], tot[r][2], tot[r][3]);
+        const float4 a = *reinterpret_cast<const float4*>(p);
+        const float2 b = *reinterpret_cast<const float2*>(p + 4);
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y;
     }
 }
 
-// split-K reduction: fixed segment order -> deterministic
-__global__ void __launch_bounds__(256) reduce_kernel(const ReduceItem* __restrict__ reds,
-                                                     const float* __restrict__ partial, Geom g,
-                                                     int tw, int th, float scale,
-                                                     float* __restrict__ out) {
-    const ReduceItem ri = reds[blockIdx.x];
-    const int X0 = ri.tx * tw, Y0 = ri.ty * th;
-    for (int e = threadIdx.x; e < tw * th; e += blockDim.x) {
-        const int r = e / tw, c = e % tw;
-        const int gy = Y0 + r, gx = X0 + c;
-        float s = 0.f;
-        for (int k = 0; k < ri.nseg; k++) s += partial[(size_t)(ri.slot0 + k) * tw * th + e];
-        if (gx < g.W && gy >= g.rb && gy < g.re) out[(size_t)(gy - g.rb) * g.W + gx] = s * scale;
+template <int MT>
+__device__ __forceinline__ void sts_mt(float* p, const float (&v)[MT]) {
+    if constexpr (MT == 3) {
+        *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+        p[2] = v[2];
+    } else if constexpr (MT == 4) {
+        *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    } else if constexpr (MT == 5) {
+        *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+        p[4] = v[4];
+    } else {
+        *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+        *reinterpret_cast<float2*>(p + 4) = make_float2(v[4], v[5]);
     }
+}
+
+// Factors of one point for units u = warp, warp + nwarps, ... of MT consecutive columns:
+// row[u*ST + e] = [c in range] * khat(c + 1/2 - P) for c = u*MT + e; ph = P - 1/2 in
+// sub-window coordinates, [lo, lo + span] the point's integer range (lo huge: no point).
+// The range test is a per-unit bitmask; the Gaussian uses the exact-ratio recurrence
+// g(d+1) = g(d) * r(d), r(d+1) = r(d) * 2^(2 kq) (2 FMUL per factor, 2 SFU ops per unit).
+template <int KERN, bool RADIAL, int MT>
+__device__ __forceinline__ void factor_units(float* row, int nunits, int warp, int nwarps, float ph,
+                                             int lo, int span, const SplatArgs& a) {
+    constexpr int ST = mt_stride<MT>();
+    for (int u = warp; u < nunits; u += nwarps) {
+        const int c0 = u * MT;
+        const int l0 = max(lo - c0, 0), h0 = min(lo + span - c0, MT - 1);
+        const uint32_t m = (l0 <= h0) ? ((2u << h0) - (1u << l0)) : 0u;
+        const float d0 = (float)c0 - ph;
+        float f[MT];
+        if (!RADIAL && KERN == 6 && a.recur) {
+            float gv = ex2_ftz(d0 * d0 * a.k.kq);
+            float r = ex2_ftz(fmaf(2.0f, d0, 1.0f) * a.k.kq);
+            const float q = a.q2;
+#pragma unroll
+            for (int e = 0; e < MT; e++) {
+                f[e] = (m & (1u << e)) ? gv : 0.f;
+                gv *= r;
+                r *= q;
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < MT; e++) {
+                const float d = d0 + (float)e;
+                if constexpr (RADIAL) f[e] = (m & (1u << e)) ? d * d * a.k.inv_h2 : __int_as_float(0x7f800000);
+                else f[e] = (m & (1u << e)) ? khat<KERN>(d, a.k) : 0.f;
+            }
+        }
+        sts_mt<MT>(row + u * ST, f);
+    }
+}
+
+// Splat pass (see the header comment).  MT x MT register micro-tile per thread; the plan
+// picks MT in {3,4,5,6} so that ceil(S/MT)^2 threads tile the sub-window S x S with full
+// warps.  Dynamic shared memory: one factor buffer of kChunk x ld floats for columns and
+// one for rows, ld = ceil(S/MT) * mt_stride + 4 (two barriers per chunk).
+template <int KERN, bool RADIAL, int MT>
+__global__ void __launch_bounds__(256) splat_kernel(const SplatArgs a) {
+    constexpr int ST = mt_stride<MT>();
+    extern __shared__ __align__(16) float smem[];
+    __shared__ int s_w, s_last;
+    const Geom& g = a.g;
+    const int ld = a.ld;
+    float* s_fx = smem;                      // [kChunk][ld]
+    float* s_fy = smem + kChunk * ld;        // [kChunk][ld]
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31, nwarps = blockDim.x >> 5;
+    const int nsub = a.nsubx * a.nsubx;
+    const int slot_floats = a.slot_ld * a.slot_ld;
+
+    for (;;) {  // persistent: items from the queue, full segments first (equal work)
+        if (t == 0) s_w = atomicAdd(&a.done[a.nslots], 1);
+        __syncthreads();
+        const int w = s_w;
+        if (w >= a.nitems) break;
+        const int4 it = a.items[w];
+        const int key = it.x, sub = it.w % nsub;
+        const int sx0 = (sub % a.nsubx) * a.S, sy0 = (sub / a.nsubx) * a.S;
+        const int Wd = g.B + 2 * g.F;
+        const int sw = min(a.S, Wd - sx0), sh = min(a.S, Wd - sy0);
+        const int bx = key % g.nbx, by = key / g.nbx;
+        const int ox = bx * g.B - g.F + sx0;  // global pixel origin of the sub-window
+        const int oy = by * g.B - g.F + sy0;
+        const int ncx = (sw + MT - 1) / MT, ncy = (sh + MT - 1) / MT;
+        const bool active = t < ncx * ncy;
+        const int mx = active ? t % ncx : 0, my = active ? t / ncx : 0;
+        // bucket-local -> sub-window coordinates (exact small-integer shift), minus 1/2
+        const float shx = (float)(bx * g.B - ox) - 0.5f, shy = (float)(by * g.B - oy) - 0.5f;
+        const uint32_t base = a.offsets[key] + (uint32_t)it.y;
+        const int cnt = it.z - it.y;
+
+        float acc[MT][MT];
+#pragma unroll
+        for (int r = 0; r < MT; r++)
+#pragma unroll
+            for (int c = 0; c < MT; c++) acc[r][c] = 0.f;
+
+        // lane p of every warp holds point p of the current chunk (coalesced, prefetched)
+        float2 nxy = make_float2(0.f, 0.f);
+        uint2 nrg = make_uint2(1u, 0u);
+        if (lane < cnt) {
+            nxy = a.xy[base + lane];
+            nrg = a.rng[base + lane];
+        }
+        const int nch = (cnt + kChunk - 1) / kChunk;
+        for (int ch = 0; ch < nch; ch++) {
+            const int np = min(kChunk, cnt - ch * kChunk);
+            const float pxh = nxy.x + shx, pyh = nxy.y + shy;
+            const int ilo = (int)(nrg.x & 0xffffu) - ox, ihi = (int)(nrg.x >> 16) - ox;
+            const int jlo = (int)(nrg.y & 0xffffu) - oy, jhi = (int)(nrg.y >> 16) - oy;
+            const bool valid = lane < np;
+            {  // prefetch the next chunk's point
+                const int q = (ch + 1) * kChunk + lane;
+                if (q < cnt) {
+                    nxy = a.xy[base + q];
+                    nrg = a.rng[base + q];
+                }
+            }
+            __syncthreads();  // previous chunk's factors consumed (and s_w read)
+            // 1-D factors of the lane's own point, MT columns (then MT rows) per unit
+            factor_units<KERN, RADIAL, MT>(s_fx + lane * ld, ncx, warp, nwarps, pxh,
+                                           valid ? ilo : (1 << 29), ihi - ilo, a);
+            factor_units<KERN, RADIAL, MT>(s_fy + lane * ld, ncy, warp, nwarps, pyh,
+                                           valid ? jlo : (1 << 29), jhi - jlo, a);
+            __syncthreads();
+            if (active) {
+                const float* fxp = s_fx + mx * ST;
+                const float* fyp = s_fy + my * ST;
+#pragma unroll 4
+                for (int p = 0; p < np; p++) {
+                    float vx[MT], vy[MT];
+                    lds_mt<MT>(fxp + p * ld, vx);
+                    lds_mt<MT>(fyp + p * ld, vy);
+#pragma unroll
+                    for (int r = 0; r < MT; r++)
+#pragma unroll
+                        for (int c = 0; c < MT; c++) {
+                            if constexpr (RADIAL) {
+                                const float r2 = vx[c] + vy[r];
+                                acc[r][c] += (r2 <= a.c2) ? khat_r<KERN>(r2) : 0.f;
+                            } else {
+                                acc[r][c] = fmaf(vy[r], vx[c], acc[r][c]);
+                            }
+                        }
+                }
+            }
+        }
+        if (active) {
+            float* sp = a.splat + (size_t)it.w * slot_floats + (my * MT) * a.slot_ld + mx * MT;
+#pragma unroll
+            for (int r = 0; r < MT; r++)
+#pragma unroll
+                for (int c = 0; c < MT; c++) sp[r * a.slot_ld + c] = acc[r][c];
+        }
+        // split group: the last segment to arrive sums all segments IN ORDER into
+        // segment 0's slot (deterministic whichever CTA does it)
+        const int2 gr = a.group[key];
+        if (gr.y > 1) {
+            __threadfence();
+            __syncthreads();
+            const int slot0 = gr.x + sub;
+            if (t == 0) s_last = (atomicAdd(&a.done[slot0], 1) == gr.y - 1);
+            __syncthreads();
+            if (s_last) {
+                __threadfence();
+                float* d0 = a.splat + (size_t)slot0 * slot_floats;
+                for (int e = t; e < slot_floats; e += blockDim.x) {
+                    float v = __ldcg(d0 + e);
+                    for (int k = 1; k < gr.y; k++) v += __ldcg(d0 + (size_t)k * nsub * slot_floats + e);
+                    d0[e] = v;
+                }
+            }
+        }
+    }
+}
+
+// Combine pass: out(i,j) = scale * sum, in order, of the splat blocks covering (i,j).
+// One CTA per 32x32 tile.  Warp 0 lists the (slot, sub-window origin, size) entries of
+// the non-empty groups whose window meets the tile -- group row-major, then sub-window
+// (row-major) -- at most ((32 + Wd)/B + 2)^2 groups x 4 sub-windows (checked at create);
+// then every thread (column t&31, rows (t>>5)+8k) walks the list kBatch entries at a time
+// so that 4 x kBatch independent loads are in flight.
+constexpr int kMaxEnt = 2048;
+constexpr int kBatch = 4;
+
+struct CombineArgs {
+    Geom g;
+    const int2* __restrict__ group;
+    const float* __restrict__ splat;
+    float* __restrict__ out;
+    const unsigned long long* __restrict__ stats;  // n_finite = stats[0] (device)
+    int nsubx, S, slot_ld;  // sub-windows per side, sub-window edge, slot edge
+    double c_over_h2;       // kernel constant / h_px^2: scale = c_over_h2 / n_finite
+};
+
+__global__ void __launch_bounds__(256) combine_kernel(const CombineArgs a) {
+    __shared__ int4 s_ent[kMaxEnt];
+    __shared__ int s_n;
+    const Geom& g = a.g;
+    const int X0 = blockIdx.x * kCombTile, Y0 = g.rb + blockIdx.y * kCombTile;
+    const int Y1 = min(Y0 + kCombTile, g.re) - 1, X1 = X0 + kCombTile - 1;
+    const int B = g.B, F = g.F, Wd = B + 2 * F, S = a.S, nsubx = a.nsubx;
+    const int bxa = max(floor_div(X0 - F, B), 0), bxb = min(floor_div(X1 + F, B), g.nbx - 1);
+    const int bya = max(floor_div(Y0 - F, B), 0), byb = min(floor_div(Y1 + F, B), g.nby - 1);
+    const int nbxr = bxb - bxa + 1, ng = nbxr * (byb - bya + 1);
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x < 32) {
+        int n = 0;
+        for (int gi0 = 0; gi0 < ng; gi0 += 32) {
+            const int gi = gi0 + lane;
+            const int by = bya + gi / nbxr, bx = bxa + gi % nbxr;
+            int2 gr = make_int2(0, 0);
+            if (gi < ng) gr = a.group[by * g.nbx + bx];
+            const int wx0 = bx * B - F, wy0 = by * B - F;
+            // sub-windows of this group meeting the tile
+            const int sxa = max(X0 - wx0, 0) / S, sxb = min(min(X1 - wx0, Wd - 1) / S, nsubx - 1);
+            const int sya = max(Y0 - wy0, 0) / S, syb = min(min(Y1 - wy0, Wd - 1) / S, nsubx - 1);
+            const int nx = (gr.y > 0 && X1 >= wx0) ? sxb - sxa + 1 : 0;
+            const int ny = (gr.y > 0 && Y1 >= wy0) ? syb - sya + 1 : 0;
+            const int cntl = (nx > 0 && ny > 0) ? nx * ny : 0;
+            int incl = cntl;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            int pos = n + incl - cntl;
+            for (int sy = 0; sy < ny; sy++)
+                for (int sx = 0; sx < nx; sx++) {
+                    const int ssx = sxa + sx, ssy = sya + sy;
+                    const int sw = min(S, Wd - ssx * S), sh = min(S, Wd - ssy * S);
+                    if (pos < kMaxEnt)
+                        s_ent[pos] = make_int4(gr.x + ssy * nsubx + ssx, wx0 + ssx * S,
+                                               wy0 + ssy * S, sw | (sh << 16));
+                    pos++;
+                }
+            n += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) s_n = min(n, kMaxEnt);
+    }
+    __syncthreads();
+    const int n = s_n;
+    const int i = X0 + lane;
+    const int jb = Y0 + (threadIdx.x >> 5);
+    const int sl = a.slot_ld;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int e0 = 0; e0 < n; e0 += kBatch) {
+        float v[kBatch][4];
+#pragma unroll
+        for (int b = 0; b < kBatch; b++) {
+            const int e = e0 + b;
+            const int4 en = e < n ? s_ent[e] : make_int4(0, 0, 0, 0);
+            const int li = i - en.y;
+            const bool inx = e < n && (unsigned)li < (unsigned)(en.w & 0xffff);
+            const float* sp = a.splat + (size_t)en.x * (sl * sl) + li;
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const int lj = jb + 8 * k - en.z;
+                v[b][k] = (inx && (unsigned)lj < (unsigned)(en.w >> 16)) ? sp[lj * sl] : 0.f;
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < kBatch; b++)
+#pragma unroll
+            for (int k = 0; k < 4; k++) acc[k] += v[b][k];
+    }
+    if (i >= g.W) return;
+    const unsigned long long nf = a.stats[0];
+    const float scale = nf ? (float)(a.c_over_h2 / (double)nf) : 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const int j = jb + 8 * k;
+        if (j <= Y1) a.out[(size_t)(j - g.rb) * g.W + i] = acc[k] * scale;
+    }
+}
+
+template <int K, bool RAD, int MT>
+static void launch_mt(const SplatArgs& a, int grid, int threads, cudaStream_t s) {
+    const size_t smem = sizeof(float) * 2 * kChunk * a.ld;
+    splat_kernel<K, RAD, MT><<<grid, threads, smem, s>>>(a);
+}
+
+template <int K, bool RAD, int MT>
+static int occ_mt(int threads, size_t smem) {
+    int nb = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, splat_kernel<K, RAD, MT>, threads, smem);
+    return nb > 0 ? nb : 1;
 }
 
 template <int K, bool RAD>
-static void launch_one(const DirectArgs& a, int nitems, cudaStream_t s) {
-    direct_kernel<K, RAD><<<nitems, 256, 0, s>>>(a);
+static int launch_one(const SplatArgs& a, int mt, int grid, int threads, cudaStream_t s) {
+    const size_t smem = sizeof(float) * 2 * kChunk * a.ld;
+    if (grid <= 0) {  // query: persistent CTAs per SM
+        switch (mt) {
+        case 3: return occ_mt<K, RAD, 3>(threads, smem);
+        case 4: return occ_mt<K, RAD, 4>(threads, smem);
+        case 5: return occ_mt<K, RAD, 5>(threads, smem);
+        default: return occ_mt<K, RAD, 6>(threads, smem);
+        }
+    }
+    switch (mt) {
+    case 3: launch_mt<K, RAD, 3>(a, grid, threads, s); break;
+    case 4: launch_mt<K, RAD, 4>(a, grid, threads, s); break;
+    case 5: launch_mt<K, RAD, 5>(a, grid, threads, s); break;
+    default: launch_mt<K, RAD, 6>(a, grid, threads, s); break;
+    }
+    return 0;
 }
 
-using LaunchFn = void (*)(const DirectArgs&, int, cudaStream_t);
-static const LaunchFn kDirect[2][8] = {
+using LaunchFn = int (*)(const SplatArgs&, int, int, int, cudaStream_t);
+static const LaunchFn kSplat[2][8] = {
     {launch_one<0, false>, launch_one<1, false>, launch_one<2, false>, launch_one<3, false>,
      launch_one<4, false>, launch_one<5, false>, launch_one<6, false>, launch_one<7, false>},
     {launch_one<0, true>, launch_one<1, true>, launch_one<2, true>, launch_one<3, true>,
@@ -287,35 +399,60 @@ KConst make_kconst(double hpx) {
     return k;
 }
 
-float make_scale(const kde_ctx* c) {
-    const double n = (double)c->stats.n_finite;
-    if (n <= 0) return 0.f;
-    return (float)(kernel_constant(c->kern, c->radial) / (n * c->hpx * c->hpx));
+int launch_combine(kde_ctx* c, float* out, cudaStream_t s) {
+    const Geom& g = c->g;
+    const EvalPlan& pl = c->plan;
+    CombineArgs a;
+    a.g = g;
+    a.group = pl.d_group;
+    a.splat = pl.d_splat;
+    a.out = out;
+    a.stats = c->d_stats;
+    a.nsubx = pl.nsubx;
+    a.S = pl.S;
+    a.slot_ld = pl.slot_ld;
+    a.c_over_h2 = kernel_constant(c->kern, c->radial) / (c->hpx * c->hpx);
+    dim3 grid((g.W + kCombTile - 1) / kCombTile, (g.re - g.rb + kCombTile - 1) / kCombTile);
+    combine_kernel<<<grid, 256, 0, s>>>(a);
+    c->launches += 1;
+    return KDE_OK;
 }
 
 int launch_direct(kde_ctx* c, float* out, cudaStream_t s) {
-    EvalPlan& pl = c->plan_dir;
-    const size_t rows = (size_t)(c->g.re - c->g.rb);
-    if (pl.any_empty || pl.items.empty())
-        cudaMemsetAsync(out, 0, rows * c->g.W * sizeof(float), s);
-    if (!pl.items.empty()) {
-        DirectArgs a;
+    EvalPlan& pl = c->plan;
+    if (pl.nitems > 0) {
+        SplatArgs a;
         a.g = c->g;
         a.offsets = c->d_offsets;
         a.xy = c->pb.xy;
         a.rng = c->pb.rng;
         a.items = pl.d_items;
-        a.out = out;
-        a.partial = pl.d_partial;
+        a.group = pl.d_group;
+        a.done = pl.d_done;
+        a.splat = pl.d_splat;
+        a.nitems = pl.nitems;
+        a.nslots = pl.nslots;
+        a.nsubx = pl.nsubx;
+        a.S = pl.S;
         a.k = make_kconst(c->hpx);
         a.c2 = (float)(c->ceff * c->ceff);
-        a.scale = make_scale(c);
-        kDirect[c->radial ? 1 : 0][c->kern](a, (int)pl.items.size(), s);
-        c->launches += 1 + (pl.reds.empty() ? 0 : 1);
-        if (!pl.reds.empty())
-            reduce_kernel<<<(int)pl.reds.size(), 256, 0, s>>>(pl.d_reds, pl.d_partial, c->g, kT, kT,
-                                                             a.scale, out);
+        a.ld = pl.ld;
+        a.slot_ld = pl.slot_ld;
+        a.q2 = (float)exp2(2.0 * (double)a.k.kq);
+        a.recur = -(double)a.k.kq * (c->g.R + 8.0) * (c->g.R + 8.0) < 120.0;
+        LaunchFn fn = kSplat[c->radial ? 1 : 0][c->kern];
+        if (pl.grid <= 0 || pl.grid_mt != pl.mt) {
+            int nsm = 148;
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->p.device);
+            pl.grid = nsm * fn(a, pl.mt, 0, pl.threads, s);
+            pl.grid_mt = pl.mt;
+        }
+        // arrival counters + queue head (done[nslots]) start at zero
+        cudaMemsetAsync(pl.d_done, 0, sizeof(int) * ((size_t)pl.nslots + 1), s);
+        fn(a, pl.mt, pl.nitems < pl.grid ? pl.nitems : pl.grid, pl.threads, s);
+        c->launches += 1;
     }
+    launch_combine(c, out, s);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "direct eval launch");
     return KDE_OK;

@@ -12,13 +12,11 @@
 
 namespace kde {
 
-constexpr int kBucket = 32;       // bucket edge B (pixels); divides every tile edge
-constexpr int kDirTile = 64;      // direct-path tile edge (pixels)
-constexpr int kSegCands = 8192;   // direct split-K: candidates per work item (fixed ->
-                                  // plan is invariant under band sharding)
-constexpr int kTcM = 128;         // tensor-core tile rows (TMEM lanes)
-constexpr int kTcN = 256;         // tensor-core tile columns (TMEM fp32 columns)
-constexpr int kTcSegCands = 16384;
+constexpr int kSub = 64;          // splat sub-window edge (pixels): one CTA, <= 256 threads
+constexpr int kSegPts = 512;      // split-K: points per splat work item (a constant, so the
+                                  // plan is invariant under band sharding);
+                                  // also bounds every fp32 running sum to 512 terms (R10)
+constexpr int kCombTile = 32;     // combine-pass output tile edge
 
 // Geometry shared by every kernel (passed by value).
 struct Geom {
@@ -26,23 +24,12 @@ struct Geom {
     double R;             // support half-width in pixels, c_eff * h/res (fp64)
     int W, H;             // raster
     int rb, re;           // band rows [rb, re)
+    int B;                // bucket (point group) edge in pixels
+    int F;                // floor(R + 1/2): window half-extent beyond the bucket (pixels)
     int nbx, nby;         // bucket grid
     int reach;            // ceil(R + 1/2) + 1 (pixels)
     int nr;               // neighbourhood radius in buckets, ceil(reach / B)
     int band_lo, band_hi; // kept bucket rows (home-bucket band filter)
-};
-
-// One CTA of an evaluation pass: tile (tx, ty), candidate positions [k0, k1) of the
-// tile's neighbourhood list, partial slot (-1: write scaled result to the raster).
-struct WorkItem {
-    int tx, ty;
-    int k0, k1;
-    int slot;
-    int pad_;
-};
-struct ReduceItem {
-    int tx, ty;
-    int slot0, nseg;
 };
 
 // Point-sized device buffers (capacity grows, never shrinks).
@@ -61,17 +48,27 @@ struct PointBufs {
 };
 
 struct EvalPlan {
-    int ntx = 0, nty0 = 0, nty1 = 0;           // tile columns, tile rows [nty0, nty1)
-    std::vector<WorkItem> items;
-    std::vector<ReduceItem> reds;
-    int nslots = 0;
-    bool any_empty = false;
-    WorkItem* d_items = nullptr;
-    int d_items_cap = 0;
-    ReduceItem* d_reds = nullptr;
-    int d_reds_cap = 0;
-    float* d_partial = nullptr;
-    int64_t partial_cap = 0;                   // floats
+    // geometry of the splat pass (fixed at create)
+    int nsubx = 1;                             // sub-windows per window side
+    int S = 1;                                 // sub-window edge (pixels)
+    int mt = 4;                                // splat register micro-tile edge
+    int slot_ld = 4;                           // splat slot edge: ceil(S/mt)*mt
+    int ld = 8;                                // factor row stride (floats)
+    int threads = 32;                          // splat CTA size
+    int grid = 0;                              // persistent splat grid (0: not yet queried)
+    int grid_mt = 0;
+    // per-load totals (read back once)
+    int tf = 0, tp = 0, nslots = 0, nitems = 0;
+    // device buffers
+    uint32_t *d_full = nullptr, *d_part = nullptr, *d_nseg = nullptr;  // nb + 1 each
+    uint32_t* d_scan_tmp = nullptr;
+    int2* d_group = nullptr;                   // per bucket: (slot of segment 0, #segments)
+    int* d_totals = nullptr;                   // TF, TP, nslots, -
+    int4* d_items = nullptr;                   // (bucket, k0, k1, slot)
+    int64_t items_cap = 0;
+    float* d_splat = nullptr;
+    int* d_done = nullptr;                     // per slot: arrivals (segment reduce); [nslots] = queue
+    int64_t slots_cap = 0;
 };
 
 }  // namespace kde
@@ -86,11 +83,12 @@ struct kde_ctx {
     kde::PointBufs pb;
     uint32_t* d_offsets = nullptr;             // nb + 1
     unsigned long long* d_stats = nullptr;     // n_finite, n_outside, useful_pairs
-    std::vector<uint32_t> h_offsets;
+    cudaEvent_t loaded_ev = nullptr;           // end of the last load (eval waits on it)
+    int* h_totals = nullptr;                   // pinned: plan totals + stats readback
     kde_stats stats{};
     bool loaded = false;
     int64_t launches = 0;                      // kernels launched (kde_stats.kernel_launches)
-    kde::EvalPlan plan_dir, plan_tc;
+    kde::EvalPlan plan;
 };
 
 namespace kde {
@@ -103,6 +101,8 @@ int bin_points(kde_ctx* c, const double* d_x, const double* d_y, int64_t n);
 // evaluation (eval_direct.cu, eval_tc.cu)
 int launch_direct(kde_ctx* c, float* out, cudaStream_t s);
 int launch_tc(kde_ctx* c, float* out, cudaStream_t s);
-int build_plan(kde_ctx* c, int tile_w, int tile_h, int seg, EvalPlan& pl, int64_t slot_floats);
+// planning (plan.cu)
+int plan_device(kde_ctx* c);
+int plan_scatter(kde_ctx* c);
 
 }  // namespace kde

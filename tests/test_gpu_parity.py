@@ -69,6 +69,15 @@ def test_binning_bit_exact(name, rows):
     np.testing.assert_array_equal(got["lx"].view(np.uint32), want["lx"].view(np.uint32))
     np.testing.assert_array_equal(got["ly"].view(np.uint32), want["ly"].view(np.uint32))
     assert got["stats"]["reach_px"] == oracle.reach_px(_grid(c))
+    # every kept window lies inside its group's window [bx*B - F, bx*B + B - 1 + F]
+    # (the splat pass relies on it; F = floor(R + 1/2))
+    B = got["stats"]["bucket"]
+    F = int(np.floor(oracle.r_px(_grid(c)) + 0.5))
+    keys = np.repeat(np.arange(len(got["offsets"]) - 1), np.diff(got["offsets"]))
+    bx, by = keys % got["stats"]["nbx"], keys // got["stats"]["nbx"]
+    r = got["ranges"]
+    assert np.all(r[:, 0] >= bx * B - F) and np.all(r[:, 1] <= bx * B + B - 1 + F)
+    assert np.all(r[:, 2] >= by * B - F) and np.all(r[:, 3] <= by * B + B - 1 + F)
 
 
 def test_binning_host_and_device_inputs_identical():
