@@ -203,16 +203,21 @@ def run_ours(args):
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms = sum(step_ms) / len(step_ms)
 
-    # --- dominant kernel: eval alone (a3/a4 + a5), events on the same stream
-    evk = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
+    # --- per-phase device times (CUDA events recorded by libkde on the streams its
+    # kernels run on), for the dominant kernel's roofline
+    k.set_timing(True)
+    ph = {"bin_ms": [], "plan_ms": [], "main_ms": [], "combine_ms": []}
     for i in range(args.steps):
         flush.zero_()
-        evk[i][0].record(stream)
+        torch.cuda.synchronize()
+        k.load(xd, yd)
         k.eval(path, out)
-        evk[i][1].record(stream)
-    torch.cuda.synchronize()
-    eval_ms = sum(a.elapsed_time(b) for a, b in evk) / args.steps
+        t = k.timing()
+        for key in ph:
+            ph[key].append(t[key])
+    k.set_timing(False)
+    phases = {key: round(sum(v) / len(v), 4) for key, v in ph.items()}
+    eval_ms = phases["main_ms"]
 
     # --- e2e: same step through the public API with HOST buffers (pinned), incl. the
     # H2D of the points and the D2H of the raster.
@@ -265,20 +270,20 @@ def run_ours(args):
         # ALU-bound: 1 FFMA (2 flops) per useful pair; FP32 peak = 148 SMs x 128 FFMA/clk
         # x 2 flops x max SM clock
         peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-        roof = {"bound": "alu", "kernel": "direct_kernel<6,false>",
+        roof = {"bound": "alu", "kernel": "splat_kernel",
                 "achieved": 2.0 * st["useful_pairs"] / (eval_ms * 1e-3) / 1e12,
                 "peak": round(peak, 2), "unit": "TFLOP/s",
                 "peak_source": "derived: 148 SMs x 128 FP32 FMA/clk x 2 x sm_max_mhz (%s)" % peak_src}
     else:
         peak = peaks["bf16_tflops"]  # fp16 dense = bf16 dense rate (guide's nominal ratio 1)
-        roof = {"bound": "tensor", "kernel": "tc_gauss_kernel",
+        roof = {"bound": "tensor", "kernel": "tc_splat_kernel",
                 "achieved": 2.0 * st["useful_pairs"] / (eval_ms * 1e-3) / 1e12,
                 "peak": peak, "unit": "TFLOP/s",
                 "peak_source": f"{peak_src} bf16_tflops (fp16 dense rate = bf16)"}
     roof["achieved"] = round(roof["achieved"], 3)
     roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
     roof["traffic"] = _traffic(roof["kernel"])
-    roof["eval_ms"] = round(eval_ms, 4)
+    roof["kernel_ms"] = round(eval_ms, 4)
 
     line = {
         "metric": METRIC, "value": useful / (ms * 1e-3), "unit": UNIT, "n_gpus": ws,
@@ -297,6 +302,7 @@ def run_ours(args):
                 "h2d_bytes_per_step": 16 * cfg["n"],
                 "d2h_bytes_per_step": 4 * W * H},
         "gpu_launches": int(launches),
+        "phases_ms": phases,
         "clocks": clocks,
         "roofline": roof,
     }

@@ -168,6 +168,22 @@ KDE_API int kde_get_stats(const kde_ctx* c, kde_stats* s);
 KDE_API int kde_get_bins(const kde_ctx* c, int64_t* offsets, int64_t* perm, float* lx, float* ly,
                  int32_t* ranges);
 
+/*
+ * Phase timing (CUDA events recorded on the streams the kernels run on), for the
+ * benchmark's roofline: disabled by default; when enabled every load/eval records
+ * events around its phases.  kde_get_timing synchronises on the last eval.
+ *   bin_ms      a1 + a2 (convert, counting sort, gather) of the last load
+ *   plan_ms     device-side plan of the last load
+ *   main_ms     the evaluation kernel of the last eval (splat pass / tensor-core pass)
+ *   combine_ms  the combine pass (a5) of the last eval
+ * Errors: KDE_EINVAL (NULL), KDE_ESTATE (timing disabled or nothing recorded).
+ */
+typedef struct {
+    float bin_ms, plan_ms, main_ms, combine_ms;
+} kde_timing;
+KDE_API int kde_set_timing(kde_ctx* c, int enable);
+KDE_API int kde_get_timing(kde_ctx* c, kde_timing* t);
+
 /* Thread-local message describing the last non-OK return on this thread. */
 KDE_API const char* kde_last_error(void);
 

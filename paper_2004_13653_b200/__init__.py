@@ -16,11 +16,12 @@ from . import _lib
 from ._lib import (KDE_COSINE, KDE_EPANECHNIKOV, KDE_GAUSSIAN, KDE_PATH_DIRECT,
                    KDE_PATH_TENSOR, KDE_QUARTIC, KDE_RADIAL, KDE_TRIANGULAR, KDE_TRICUBE,
                    KDE_TRIWEIGHT, KDE_UNIFORM, KERNEL_NAMES, KdeError, kde_create, kde_eval,
-                   kde_free, kde_get_bins, kde_get_stats, kde_last_error, kde_load_points,
-                   kde_params)
+                   kde_free, kde_get_bins, kde_get_stats, kde_get_timing, kde_last_error,
+                   kde_load_points, kde_params, kde_set_timing)
 
 __all__ = ["KDE", "KdeError", "kde_params", "kde_create", "kde_load_points", "kde_eval",
-           "kde_get_stats", "kde_get_bins", "kde_last_error", "kde_free", "KERNEL_NAMES",
+           "kde_get_stats", "kde_get_bins", "kde_set_timing", "kde_get_timing", "kde_last_error",
+           "kde_free", "KERNEL_NAMES",
            "KDE_PATH_DIRECT", "KDE_PATH_TENSOR", "KDE_RADIAL", "kernel_id"]
 
 
@@ -66,6 +67,12 @@ class KDE:
 
     def bins(self):
         return kde_get_bins(self.ctx)
+
+    def set_timing(self, enable=True):
+        kde_set_timing(self.ctx, enable)
+
+    def timing(self):
+        return kde_get_timing(self.ctx)
 
     def close(self):
         if getattr(self, "ctx", None):

@@ -26,7 +26,7 @@ _CODES = {KDE_EINVAL: "EINVAL", KDE_ENOMEM: "ENOMEM", KDE_ECUDA: "ECUDA",
           KDE_EUNSUPPORTED: "EUNSUPPORTED", KDE_ESTATE: "ESTATE"}
 
 EXPORTS = ("kde_create", "kde_load_points", "kde_eval", "kde_get_stats", "kde_get_bins",
-           "kde_last_error", "kde_free")
+           "kde_set_timing", "kde_get_timing", "kde_last_error", "kde_free")
 
 
 class kde_params(ctypes.Structure):
@@ -46,6 +46,11 @@ class kde_stats(ctypes.Structure):
 
     def as_dict(self):
         return {f: int(getattr(self, f)) for f, _ in self._fields_}
+
+
+class kde_timing(ctypes.Structure):
+    _fields_ = [("bin_ms", ctypes.c_float), ("plan_ms", ctypes.c_float),
+                ("main_ms", ctypes.c_float), ("combine_ms", ctypes.c_float)]
 
 
 class KdeError(RuntimeError):
@@ -68,9 +73,12 @@ def _load():
     L.kde_get_bins.argtypes = [vp, vp, vp, vp, vp, vp]
     L.kde_last_error.restype = ctypes.c_char_p
     L.kde_last_error.argtypes = []
+    L.kde_set_timing.argtypes = [vp, ctypes.c_int]
+    L.kde_get_timing.argtypes = [vp, P(kde_timing)]
     L.kde_free.argtypes = [vp]
     L.kde_free.restype = None
-    for f in ("kde_create", "kde_load_points", "kde_eval", "kde_get_stats", "kde_get_bins"):
+    for f in ("kde_create", "kde_load_points", "kde_eval", "kde_get_stats", "kde_get_bins",
+              "kde_set_timing", "kde_get_timing"):
         getattr(L, f).restype = ctypes.c_int
     return L
 
@@ -147,6 +155,16 @@ def kde_get_bins(ctx: int) -> dict:
     _check(_L.kde_get_bins(ctx, off.ctypes.data, perm.ctypes.data, lx.ctypes.data,
                            ly.ctypes.data, rng.ctypes.data))
     return dict(offsets=off, perm=perm[:m], lx=lx[:m], ly=ly[:m], ranges=rng[:m], stats=st)
+
+
+def kde_set_timing(ctx: int, enable: bool) -> None:
+    _check(_L.kde_set_timing(ctx, 1 if enable else 0))
+
+
+def kde_get_timing(ctx: int) -> dict:
+    t = kde_timing()
+    _check(_L.kde_get_timing(ctx, ctypes.byref(t)))
+    return {f: float(getattr(t, f)) for f, _ in t._fields_}
 
 
 def kde_free(ctx: int | None) -> None:

@@ -1,6 +1,8 @@
 """Build libkde.so in-tree with nvcc for sm_100a (no JIT, no torch extension cache).
 
-    python -m paper_2004_13653_b200.build [--force]
+    python paper_2004_13653_b200/build.py [--force]
+
+(Run as a script or load by path: importing the package loads libkde.so.)
 """
 from __future__ import annotations
 

@@ -269,10 +269,14 @@ int kde_load_points(kde_ctx* c, const double* x, const double* y, int64_t n) {
             dy = c->pb.y;
         }
     }
+    tmark(c, 0, c->stream);
     int rc = bin_points(c, dx, dy, n);
     if (rc) return rc;
+    tmark(c, 1, c->stream);
     rc = plan_device(c);
     if (rc) return rc;
+    tmark(c, 2, c->stream);
+    c->tev_load = c->timing;
     // one small readback: plan totals (TF, TP, nslots, n_binned) + integer stats
     cudaMemcpyAsync(c->h_totals, c->plan.d_totals, 4 * sizeof(int), cudaMemcpyDeviceToHost, c->stream);
     cudaMemcpyAsync(c->h_totals + 4, c->d_stats, 3 * sizeof(unsigned long long),
@@ -336,6 +340,40 @@ int kde_eval(kde_ctx* c, int32_t path, float* out, void* stream) {
     e = cudaStreamWaitEvent(s, c->loaded_ev, 0);  // the plan scatter of the last load
     if (e != cudaSuccess) return cuda_fail(e, "kde_eval: wait for load");
     return path == KDE_PATH_DIRECT ? launch_direct(c, out, s) : launch_tc(c, out, s);
+}
+
+int kde_set_timing(kde_ctx* c, int enable) {
+    if (!c) {
+        set_error("kde_set_timing: NULL context");
+        return KDE_EINVAL;
+    }
+    DeviceGuard dg(c->p.device);
+    if (enable && !c->tev[0])
+        for (int k = 0; k < 6; k++)
+            if (cudaEventCreate(&c->tev[k]) != cudaSuccess) return cuda_fail(cudaGetLastError(), "kde_set_timing");
+    c->timing = enable != 0;
+    c->tev_load = c->tev_eval = false;
+    return KDE_OK;
+}
+
+int kde_get_timing(kde_ctx* c, kde_timing* t) {
+    if (!c || !t) {
+        set_error("kde_get_timing: NULL argument");
+        return KDE_EINVAL;
+    }
+    if (!c->timing || !c->tev_load || !c->tev_eval) {
+        set_error("kde_get_timing: timing disabled or no load+eval recorded since enabling");
+        return KDE_ESTATE;
+    }
+    DeviceGuard dg(c->p.device);
+    cudaError_t e = cudaEventSynchronize(c->tev[5]);
+    if (e == cudaSuccess) e = cudaEventSynchronize(c->tev[2]);
+    if (e != cudaSuccess) return cuda_fail(e, "kde_get_timing");
+    cudaEventElapsedTime(&t->bin_ms, c->tev[0], c->tev[1]);
+    cudaEventElapsedTime(&t->plan_ms, c->tev[1], c->tev[2]);
+    cudaEventElapsedTime(&t->main_ms, c->tev[3], c->tev[4]);
+    cudaEventElapsedTime(&t->combine_ms, c->tev[4], c->tev[5]);
+    return KDE_OK;
 }
 
 int kde_get_stats(const kde_ctx* c, kde_stats* s) {
@@ -423,6 +461,8 @@ void kde_free(kde_ctx* c) {
     free_plan(c->plan);
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->loaded_ev) cudaEventDestroy(c->loaded_ev);
+    for (int k = 0; k < 6; k++)
+        if (c->tev[k]) cudaEventDestroy(c->tev[k]);
     if (c->h_totals) cudaFreeHost(c->h_totals);
     delete c;
     if (prev >= 0) cudaSetDevice(prev);

@@ -449,10 +449,16 @@ int launch_direct(kde_ctx* c, float* out, cudaStream_t s) {
         }
         // arrival counters + queue head (done[nslots]) start at zero
         cudaMemsetAsync(pl.d_done, 0, sizeof(int) * ((size_t)pl.nslots + 1), s);
+        tmark(c, 3, s);
         fn(a, pl.mt, pl.nitems < pl.grid ? pl.nitems : pl.grid, pl.threads, s);
         c->launches += 1;
+    } else {
+        tmark(c, 3, s);
     }
+    tmark(c, 4, s);
     launch_combine(c, out, s);
+    tmark(c, 5, s);
+    c->tev_eval = c->timing;
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "direct eval launch");
     return KDE_OK;

@@ -88,12 +88,18 @@ struct kde_ctx {
     kde_stats stats{};
     bool loaded = false;
     int64_t launches = 0;                      // kernels launched (kde_stats.kernel_launches)
+    bool timing = false;                       // record phase events (kde_set_timing)
+    cudaEvent_t tev[6] = {};                   // bin0, bin1/plan0, plan1, main0, main1, comb1
+    bool tev_load = false, tev_eval = false;
     kde::EvalPlan plan;
 };
 
 namespace kde {
 
 void set_error(const char* fmt, ...);
+inline void tmark(kde_ctx* c, int k, cudaStream_t s) {
+    if (c->timing) cudaEventRecord(c->tev[k], s);
+}
 int cuda_fail(cudaError_t e, const char* what);
 
 // binning (bin.cu)
