@@ -51,18 +51,25 @@ static int dalloc(void** p, size_t bytes, const char* what) {
     return KDE_OK;
 }
 
-// Splat-pass geometry, fixed at create: sub-windows of the group window B + 2F, and the
-// register micro-tile edge whose thread grid best fills whole warps.
-static void plan_geometry(EvalPlan& pl, const Geom& g) {
+// Direct-path geometry, fixed at create: groups are single buckets; the window B + 2F is
+// cut into equal square sub-windows of <= kSub, and the register micro-tile edge MT is the
+// one whose thread grid best fills whole warps.
+static void plan_geometry_direct(EvalPlan& pl, const Geom& g) {
+    PathGeom& pg = pl.pg;
     const int Wd = g.B + 2 * g.F;
-    pl.nsubx = (Wd + kSub - 1) / kSub;
-    pl.S = (Wd + pl.nsubx - 1) / pl.nsubx;  // equal sub-windows (the last may be smaller)
+    pg.s = 1;
+    pg.ngx = g.nbx;
+    pg.ngy = g.nby;
+    pg.px = pg.py = g.B;
+    pg.ww = pg.wh = Wd;
+    pg.nsubx = pg.nsuby = (Wd + kSub - 1) / kSub;
+    pg.sx = pg.sy = (Wd + pg.nsubx - 1) / pg.nsubx;  // the last sub-window may be smaller
     double best = -1.0;
     for (int mt = 3; mt <= 6; mt++) {
-        const int nm = (pl.S + mt - 1) / mt;
+        const int nm = (pg.sx + mt - 1) / mt;
         if (nm * nm > 256) continue;
         const int thr = ((nm * nm + 31) / 32) * 32;
-        const double cover = (double)pl.S / (nm * mt);
+        const double cover = (double)pg.sx / (nm * mt);
         const double util = cover * cover * (double)(nm * nm) / thr + 1e-3 * mt;
         if (util > best) {
             best = util;
@@ -70,9 +77,72 @@ static void plan_geometry(EvalPlan& pl, const Geom& g) {
             pl.threads = thr;
         }
     }
-    const int nm = (pl.S + pl.mt - 1) / pl.mt;
-    pl.slot_ld = nm * pl.mt;
+    const int nm = (pg.sx + pl.mt - 1) / pl.mt;
+    pg.slot_w = pg.slot_h = nm * pl.mt;
     pl.ld = nm * (pl.mt <= 4 ? 4 : 8) + 4;
+    pl.enabled = true;
+}
+
+// Tensor-core geometry: a group is a vertical stack of s buckets whose window fills the
+// M = 128 TMEM lanes (rows); columns N = B + 2F rounded up to 16.  Product Gaussian only,
+// and only while B + 2F <= 128 (R_px <= ~56).
+static void plan_geometry_tc(EvalPlan& pl, const Geom& g, bool gaussian_product) {
+    PathGeom& pg = pl.pg;
+    const int Wd = g.B + 2 * g.F;
+    pl.enabled = gaussian_product && Wd <= kTcM;
+    if (!pl.enabled) return;
+    pg.s = std::max(1, (kTcM - 2 * g.F) / g.B);
+    pg.ngx = g.nbx;
+    pg.ngy = (g.nby + pg.s - 1) / pg.s;
+    pg.px = g.B;
+    pg.py = pg.s * g.B;
+    pg.ww = Wd;
+    pg.wh = pg.py + 2 * g.F;
+    pg.nsubx = pg.nsuby = 1;
+    pg.sx = pg.ww;
+    pg.sy = pg.wh;
+    pg.slot_w = ((Wd + 15) / 16) * 16;  // MMA N
+    pg.slot_h = kTcM;
+}
+
+static int alloc_plan(EvalPlan& pl) {
+    if (!pl.enabled) return KDE_OK;
+    const size_t ng = (size_t)pl.pg.ngroups();
+    cudaError_t e = cudaMalloc(&pl.d_full, sizeof(uint32_t) * (ng + 1));
+    if (e == cudaSuccess) e = cudaMalloc(&pl.d_part, sizeof(uint32_t) * (ng + 1));
+    if (e == cudaSuccess) e = cudaMalloc(&pl.d_nseg, sizeof(uint32_t) * (ng + 1));
+    if (e == cudaSuccess) e = cudaMalloc(&pl.d_scan_tmp, sizeof(uint32_t) * ((ng + 1) / 2048 + 2));
+    if (e == cudaSuccess) e = cudaMalloc(&pl.d_group, sizeof(int2) * (ng > 0 ? ng : 1));
+    if (e == cudaSuccess) e = cudaMalloc(&pl.d_totals, sizeof(int) * 4);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        set_error("kde_create: plan allocation failed");
+        return KDE_ENOMEM;
+    }
+    return KDE_OK;
+}
+
+// after the totals are known: item list + splat capacity, then the item scatter
+static int finish_plan(kde_ctx* c, EvalPlan& pl, const int* tot) {
+    if (!pl.enabled) return KDE_OK;
+    const int nsub = pl.pg.nsub();
+    pl.tf = tot[0];
+    pl.tp = tot[1];
+    pl.nslots = tot[2];
+    pl.nitems = (pl.tf + pl.tp) * nsub;
+    if (pl.nitems > pl.items_cap) {
+        if (dalloc((void**)&pl.d_items, sizeof(int4) * pl.nitems, "plan items")) return KDE_ENOMEM;
+        pl.items_cap = pl.nitems;
+    }
+    if (pl.nslots > pl.slots_cap) {
+        if (dalloc((void**)&pl.d_splat, sizeof(float) * (size_t)pl.nslots * pl.pg.slot_floats(),
+                   "splat blocks"))
+            return KDE_ENOMEM;
+        if (dalloc((void**)&pl.d_done, sizeof(int) * ((size_t)pl.nslots + 1), "splat counters"))
+            return KDE_ENOMEM;
+        pl.slots_cap = pl.nslots;
+    }
+    return plan_scatter(c, pl);
 }
 
 static void free_plan(EvalPlan& pl) {
@@ -194,25 +264,24 @@ int kde_create(const kde_params* p, kde_ctx** out) {
     g.band_lo = rb / g.B - g.nr;
     g.band_hi = (re - 1) / g.B + g.nr;
     const size_t nb = (size_t)g.nbx * g.nby;
-    plan_geometry(c->plan, g);
+    plan_geometry_direct(c->plan[KDE_PATH_DIRECT], g);
+    plan_geometry_tc(c->plan[KDE_PATH_TENSOR], g, kern == KDE_GAUSSIAN && !c->radial);
     // a BLOCKING stream: loads are ordered after work on the legacy default stream
     // (where device-resident inputs are usually produced, e.g. by PyTorch's default stream)
     cudaError_t e = cudaStreamCreate(&c->stream);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->loaded_ev, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaMallocHost(&c->h_totals, 64);
+    if (e == cudaSuccess) e = cudaMallocHost(&c->h_totals, 128);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_offsets, sizeof(uint32_t) * (nb + 1));
     if (e == cudaSuccess) e = cudaMalloc(&c->d_stats, sizeof(unsigned long long) * 4);
-    EvalPlan& pl = c->plan;
-    if (e == cudaSuccess) e = cudaMalloc(&pl.d_full, sizeof(uint32_t) * (nb + 1));
-    if (e == cudaSuccess) e = cudaMalloc(&pl.d_part, sizeof(uint32_t) * (nb + 1));
-    if (e == cudaSuccess) e = cudaMalloc(&pl.d_nseg, sizeof(uint32_t) * (nb + 1));
-    if (e == cudaSuccess) e = cudaMalloc(&pl.d_scan_tmp, sizeof(uint32_t) * ((nb + 1) / 2048 + 2));
-    if (e == cudaSuccess) e = cudaMalloc(&pl.d_group, sizeof(int2) * nb);
-    if (e == cudaSuccess) e = cudaMalloc(&pl.d_totals, sizeof(int) * 4);
     if (e != cudaSuccess) {
         kde_free(c);
         return cuda_fail(e, "kde_create: allocation");
     }
+    for (int p = 0; p < 2; p++)
+        if (alloc_plan(c->plan[p])) {
+            kde_free(c);
+            return KDE_ENOMEM;
+        }
     c->stats.bucket = g.B;
     c->stats.nbx = g.nbx;
     c->stats.nby = g.nby;
@@ -273,42 +342,32 @@ int kde_load_points(kde_ctx* c, const double* x, const double* y, int64_t n) {
     int rc = bin_points(c, dx, dy, n);
     if (rc) return rc;
     tmark(c, 1, c->stream);
-    rc = plan_device(c);
-    if (rc) return rc;
+    for (int p = 0; p < 2; p++)
+        if (c->plan[p].enabled) {
+            rc = plan_device(c, c->plan[p]);
+            if (rc) return rc;
+        }
     tmark(c, 2, c->stream);
     c->tev_load = c->timing;
-    // one small readback: plan totals (TF, TP, nslots, n_binned) + integer stats
-    cudaMemcpyAsync(c->h_totals, c->plan.d_totals, 4 * sizeof(int), cudaMemcpyDeviceToHost, c->stream);
-    cudaMemcpyAsync(c->h_totals + 4, c->d_stats, 3 * sizeof(unsigned long long),
+    // one small readback: plan totals of both paths + the integer stats
+    for (int p = 0; p < 2; p++)
+        if (c->plan[p].enabled)
+            cudaMemcpyAsync(c->h_totals + 4 * p, c->plan[p].d_totals, 4 * sizeof(int),
+                            cudaMemcpyDeviceToHost, c->stream);
+    cudaMemcpyAsync(c->h_totals + 8, c->d_stats, 3 * sizeof(unsigned long long),
                     cudaMemcpyDeviceToHost, c->stream);
     cudaError_t e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) return cuda_fail(e, "kde_load_points");
-    const unsigned long long* st = reinterpret_cast<const unsigned long long*>(c->h_totals + 4);
+    const unsigned long long* st = reinterpret_cast<const unsigned long long*>(c->h_totals + 8);
     c->stats.n_in = n;
     c->stats.n_finite = (int64_t)st[0];
     c->stats.n_outside = (int64_t)st[1];
     c->stats.useful_pairs = (int64_t)st[2];
     c->stats.n_binned = (int64_t)c->h_totals[3];
-    EvalPlan& pl = c->plan;
-    const int nsub = pl.nsubx * pl.nsubx;
-    pl.tf = c->h_totals[0];
-    pl.tp = c->h_totals[1];
-    pl.nslots = c->h_totals[2];
-    pl.nitems = (pl.tf + pl.tp) * nsub;
-    if (pl.nitems > pl.items_cap) {
-        if (dalloc((void**)&pl.d_items, sizeof(int4) * pl.nitems, "splat items")) return KDE_ENOMEM;
-        pl.items_cap = pl.nitems;
+    for (int p = 0; p < 2; p++) {
+        rc = finish_plan(c, c->plan[p], c->h_totals + 4 * p);
+        if (rc) return rc;
     }
-    if (pl.nslots > pl.slots_cap) {
-        if (dalloc((void**)&pl.d_splat, sizeof(float) * (size_t)pl.nslots * pl.slot_ld * pl.slot_ld,
-                   "splat blocks"))
-            return KDE_ENOMEM;
-        if (dalloc((void**)&pl.d_done, sizeof(int) * ((size_t)pl.nslots + 1), "splat counters"))
-            return KDE_ENOMEM;
-        pl.slots_cap = pl.nslots;
-    }
-    rc = plan_scatter(c);
-    if (rc) return rc;
     e = cudaEventRecord(c->loaded_ev, c->stream);
     if (e != cudaSuccess) return cuda_fail(e, "kde_load_points: event");
     c->loaded = true;
@@ -328,8 +387,9 @@ int kde_eval(kde_ctx* c, int32_t path, float* out, void* stream) {
         set_error("kde_eval: no points loaded");
         return KDE_ESTATE;
     }
-    if (path == KDE_PATH_TENSOR && (c->radial || c->kern != KDE_GAUSSIAN)) {
-        set_error("kde_eval: the tensor-core path implements the product-form Gaussian only");
+    if (path == KDE_PATH_TENSOR && !c->plan[KDE_PATH_TENSOR].enabled) {
+        set_error("kde_eval: the tensor-core path implements the product-form Gaussian with "
+                  "B + 2*floor(R+1/2) <= 128 px only");
         return KDE_EUNSUPPORTED;
     }
     DeviceGuard dg(c->p.device);
@@ -458,7 +518,8 @@ void kde_free(kde_ctx* c) {
     cudaFree(pb.rng);
     cudaFree(c->d_offsets);
     cudaFree(c->d_stats);
-    free_plan(c->plan);
+    free_plan(c->plan[0]);
+    free_plan(c->plan[1]);
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->loaded_ev) cudaEventDestroy(c->loaded_ev);
     for (int k = 0; k < 6; k++)

@@ -36,13 +36,13 @@ struct SplatArgs {
     const int2* __restrict__ group;   // per bucket: (slot of segment 0, #segments)
     int* __restrict__ done;           // per slot arrival counters; done[nslots] = work queue
     float* __restrict__ splat;
-    int nitems, nslots, nsubx, S;
+    PathGeom pg;
+    int nitems, nslots;
     KConst k;
     float c2;     // radial: c_eff^2
     float q2;     // Gaussian recurrence step 2^(2 kq)
     bool recur;   // recurrence safe: 2^(kq (R + 8)^2) stays a normal float
     int ld;       // factor row stride (floats)
-    int slot_ld;  // splat slot edge (floats): ceil(S/MT)*MT
 };
 
 constexpr int kChunk = 32;         // points per factor chunk (one per lane)
@@ -140,8 +140,8 @@ __global__ void __launch_bounds__(256) splat_kernel(const SplatArgs a) {
     float* s_fx = smem;                      // [kChunk][ld]
     float* s_fy = smem + kChunk * ld;        // [kChunk][ld]
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31, nwarps = blockDim.x >> 5;
-    const int nsub = a.nsubx * a.nsubx;
-    const int slot_floats = a.slot_ld * a.slot_ld;
+    const int nsubx = a.pg.nsubx, nsub = a.pg.nsub(), S = a.pg.sx, slot_ld = a.pg.slot_w;
+    const int slot_floats = slot_ld * slot_ld;
 
     for (;;) {  // persistent: items from the queue, full segments first (equal work)
         if (t == 0) s_w = atomicAdd(&a.done[a.nslots], 1);
@@ -150,9 +150,9 @@ __global__ void __launch_bounds__(256) splat_kernel(const SplatArgs a) {
         if (w >= a.nitems) break;
         const int4 it = a.items[w];
         const int key = it.x, sub = it.w % nsub;
-        const int sx0 = (sub % a.nsubx) * a.S, sy0 = (sub / a.nsubx) * a.S;
-        const int Wd = g.B + 2 * g.F;
-        const int sw = min(a.S, Wd - sx0), sh = min(a.S, Wd - sy0);
+        const int sx0 = (sub % nsubx) * S, sy0 = (sub / nsubx) * S;
+        const int Wd = a.pg.ww;
+        const int sw = min(S, Wd - sx0), sh = min(S, Wd - sy0);
         const int bx = key % g.nbx, by = key / g.nbx;
         const int ox = bx * g.B - g.F + sx0;  // global pixel origin of the sub-window
         const int oy = by * g.B - g.F + sy0;
@@ -221,11 +221,11 @@ __global__ void __launch_bounds__(256) splat_kernel(const SplatArgs a) {
             }
         }
         if (active) {
-            float* sp = a.splat + (size_t)it.w * slot_floats + (my * MT) * a.slot_ld + mx * MT;
+            float* sp = a.splat + (size_t)it.w * slot_floats + (my * MT) * slot_ld + mx * MT;
 #pragma unroll
             for (int r = 0; r < MT; r++)
 #pragma unroll
-                for (int c = 0; c < MT; c++) sp[r * a.slot_ld + c] = acc[r][c];
+                for (int c = 0; c < MT; c++) sp[r * slot_ld + c] = acc[r][c];
         }
         // split group: the last segment to arrive sums all segments IN ORDER into
         // segment 0's slot (deterministic whichever CTA does it)
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(256) splat_kernel(const SplatArgs a) {
         if (gr.y > 1) {
             __threadfence();
             __syncthreads();
-            const int slot0 = gr.x + sub;
+            const int slot0 = gr.x * nsub + sub;
             if (t == 0) s_last = (atomicAdd(&a.done[slot0], 1) == gr.y - 1);
             __syncthreads();
             if (s_last) {
@@ -250,46 +250,49 @@ __global__ void __launch_bounds__(256) splat_kernel(const SplatArgs a) {
 }
 
 // Combine pass: out(i,j) = scale * sum, in order, of the splat blocks covering (i,j).
-// One CTA per 32x32 tile.  Warp 0 lists the (slot, sub-window origin, size) entries of
-// the non-empty groups whose window meets the tile -- group row-major, then sub-window
-// (row-major) -- at most ((32 + Wd)/B + 2)^2 groups x 4 sub-windows (checked at create);
-// then every thread (column t&31, rows (t>>5)+8k) walks the list kBatch entries at a time
-// so that 4 x kBatch independent loads are in flight.
+// Works for any path geometry (groups of pitch px x py, windows ww x wh, sub-windows).
+// One CTA per 32x32 tile.  Warp 0 lists the (slot, sub-window origin, size) entries of the
+// non-empty groups whose window meets the tile -- group row-major, then sub-window
+// (row-major) -- at most ((32 + ww)/px + 2)((32 + wh)/py + 2) groups x 4 sub-windows
+// (checked at create); then every thread (column t&31, rows (t>>5)+8k) walks the list
+// kBatch entries at a time so that 4 x kBatch independent loads are in flight.
 constexpr int kMaxEnt = 2048;
 constexpr int kBatch = 4;
 
 struct CombineArgs {
     Geom g;
-    const int2* __restrict__ group;
+    PathGeom pg;
+    const int2* __restrict__ group;  // per group: (first segment, #segments)
     const float* __restrict__ splat;
     float* __restrict__ out;
     const unsigned long long* __restrict__ stats;  // n_finite = stats[0] (device)
-    int nsubx, S, slot_ld;  // sub-windows per side, sub-window edge, slot edge
-    double c_over_h2;       // kernel constant / h_px^2: scale = c_over_h2 / n_finite
+    double c_over_h2;  // kernel constant / h_px^2: scale = c_over_h2 / n_finite
 };
 
 __global__ void __launch_bounds__(256) combine_kernel(const CombineArgs a) {
     __shared__ int4 s_ent[kMaxEnt];
     __shared__ int s_n;
     const Geom& g = a.g;
+    const PathGeom& pg = a.pg;
     const int X0 = blockIdx.x * kCombTile, Y0 = g.rb + blockIdx.y * kCombTile;
     const int Y1 = min(Y0 + kCombTile, g.re) - 1, X1 = X0 + kCombTile - 1;
-    const int B = g.B, F = g.F, Wd = B + 2 * F, S = a.S, nsubx = a.nsubx;
-    const int bxa = max(floor_div(X0 - F, B), 0), bxb = min(floor_div(X1 + F, B), g.nbx - 1);
-    const int bya = max(floor_div(Y0 - F, B), 0), byb = min(floor_div(Y1 + F, B), g.nby - 1);
-    const int nbxr = bxb - bxa + 1, ng = nbxr * (byb - bya + 1);
+    const int F = g.F;
+    const int gxa = max(floor_div(X0 - F, pg.px), 0), gxb = min(floor_div(X1 + F, pg.px), pg.ngx - 1);
+    const int gya = max(floor_div(Y0 - F, pg.py), 0), gyb = min(floor_div(Y1 + F, pg.py), pg.ngy - 1);
+    const int ngxr = gxb - gxa + 1, ng = ngxr * (gyb - gya + 1);
+    const int nsub = pg.nsub();
     const int lane = threadIdx.x & 31;
     if (threadIdx.x < 32) {
         int n = 0;
         for (int gi0 = 0; gi0 < ng; gi0 += 32) {
             const int gi = gi0 + lane;
-            const int by = bya + gi / nbxr, bx = bxa + gi % nbxr;
+            const int gy = gya + gi / ngxr, gx = gxa + gi % ngxr;
             int2 gr = make_int2(0, 0);
-            if (gi < ng) gr = a.group[by * g.nbx + bx];
-            const int wx0 = bx * B - F, wy0 = by * B - F;
+            if (gi < ng) gr = a.group[gy * pg.ngx + gx];
+            const int wx0 = gx * pg.px - F, wy0 = gy * pg.py - F;
             // sub-windows of this group meeting the tile
-            const int sxa = max(X0 - wx0, 0) / S, sxb = min(min(X1 - wx0, Wd - 1) / S, nsubx - 1);
-            const int sya = max(Y0 - wy0, 0) / S, syb = min(min(Y1 - wy0, Wd - 1) / S, nsubx - 1);
+            const int sxa = max(X0 - wx0, 0) / pg.sx, sxb = min(min(X1 - wx0, pg.ww - 1) / pg.sx, pg.nsubx - 1);
+            const int sya = max(Y0 - wy0, 0) / pg.sy, syb = min(min(Y1 - wy0, pg.wh - 1) / pg.sy, pg.nsuby - 1);
             const int nx = (gr.y > 0 && X1 >= wx0) ? sxb - sxa + 1 : 0;
             const int ny = (gr.y > 0 && Y1 >= wy0) ? syb - sya + 1 : 0;
             const int cntl = (nx > 0 && ny > 0) ? nx * ny : 0;
@@ -303,10 +306,10 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineArgs a) {
             for (int sy = 0; sy < ny; sy++)
                 for (int sx = 0; sx < nx; sx++) {
                     const int ssx = sxa + sx, ssy = sya + sy;
-                    const int sw = min(S, Wd - ssx * S), sh = min(S, Wd - ssy * S);
+                    const int sw = min(pg.sx, pg.ww - ssx * pg.sx), sh = min(pg.sy, pg.wh - ssy * pg.sy);
                     if (pos < kMaxEnt)
-                        s_ent[pos] = make_int4(gr.x + ssy * nsubx + ssx, wx0 + ssx * S,
-                                               wy0 + ssy * S, sw | (sh << 16));
+                        s_ent[pos] = make_int4(gr.x * nsub + ssy * pg.nsubx + ssx, wx0 + ssx * pg.sx,
+                                               wy0 + ssy * pg.sy, sw | (sh << 16));
                     pos++;
                 }
             n += __shfl_sync(0xffffffffu, incl, 31);
@@ -317,7 +320,8 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineArgs a) {
     const int n = s_n;
     const int i = X0 + lane;
     const int jb = Y0 + (threadIdx.x >> 5);
-    const int sl = a.slot_ld;
+    const int sl = pg.slot_w;
+    const size_t sf = (size_t)pg.slot_floats();
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
     for (int e0 = 0; e0 < n; e0 += kBatch) {
         float v[kBatch][4];
@@ -327,11 +331,11 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineArgs a) {
             const int4 en = e < n ? s_ent[e] : make_int4(0, 0, 0, 0);
             const int li = i - en.y;
             const bool inx = e < n && (unsigned)li < (unsigned)(en.w & 0xffff);
-            const float* sp = a.splat + (size_t)en.x * (sl * sl) + li;
+            const float* sp = a.splat + (size_t)en.x * sf + li;
 #pragma unroll
             for (int k = 0; k < 4; k++) {
                 const int lj = jb + 8 * k - en.z;
-                v[b][k] = (inx && (unsigned)lj < (unsigned)(en.w >> 16)) ? sp[lj * sl] : 0.f;
+                v[b][k] = (inx && (unsigned)lj < (unsigned)(en.w >> 16)) ? sp[(size_t)lj * sl] : 0.f;
             }
         }
 #pragma unroll
@@ -399,18 +403,15 @@ KConst make_kconst(double hpx) {
     return k;
 }
 
-int launch_combine(kde_ctx* c, float* out, cudaStream_t s) {
+int launch_combine(kde_ctx* c, const EvalPlan& pl, float* out, cudaStream_t s) {
     const Geom& g = c->g;
-    const EvalPlan& pl = c->plan;
     CombineArgs a;
     a.g = g;
+    a.pg = pl.pg;
     a.group = pl.d_group;
     a.splat = pl.d_splat;
     a.out = out;
     a.stats = c->d_stats;
-    a.nsubx = pl.nsubx;
-    a.S = pl.S;
-    a.slot_ld = pl.slot_ld;
     a.c_over_h2 = kernel_constant(c->kern, c->radial) / (c->hpx * c->hpx);
     dim3 grid((g.W + kCombTile - 1) / kCombTile, (g.re - g.rb + kCombTile - 1) / kCombTile);
     combine_kernel<<<grid, 256, 0, s>>>(a);
@@ -419,7 +420,7 @@ int launch_combine(kde_ctx* c, float* out, cudaStream_t s) {
 }
 
 int launch_direct(kde_ctx* c, float* out, cudaStream_t s) {
-    EvalPlan& pl = c->plan;
+    EvalPlan& pl = c->plan[KDE_PATH_DIRECT];
     if (pl.nitems > 0) {
         SplatArgs a;
         a.g = c->g;
@@ -430,22 +431,19 @@ int launch_direct(kde_ctx* c, float* out, cudaStream_t s) {
         a.group = pl.d_group;
         a.done = pl.d_done;
         a.splat = pl.d_splat;
+        a.pg = pl.pg;
         a.nitems = pl.nitems;
         a.nslots = pl.nslots;
-        a.nsubx = pl.nsubx;
-        a.S = pl.S;
         a.k = make_kconst(c->hpx);
         a.c2 = (float)(c->ceff * c->ceff);
         a.ld = pl.ld;
-        a.slot_ld = pl.slot_ld;
         a.q2 = (float)exp2(2.0 * (double)a.k.kq);
         a.recur = -(double)a.k.kq * (c->g.R + 8.0) * (c->g.R + 8.0) < 120.0;
         LaunchFn fn = kSplat[c->radial ? 1 : 0][c->kern];
-        if (pl.grid <= 0 || pl.grid_mt != pl.mt) {
+        if (pl.grid <= 0) {
             int nsm = 148;
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->p.device);
             pl.grid = nsm * fn(a, pl.mt, 0, pl.threads, s);
-            pl.grid_mt = pl.mt;
         }
         // arrival counters + queue head (done[nslots]) start at zero
         cudaMemsetAsync(pl.d_done, 0, sizeof(int) * ((size_t)pl.nslots + 1), s);
@@ -456,7 +454,7 @@ int launch_direct(kde_ctx* c, float* out, cudaStream_t s) {
         tmark(c, 3, s);
     }
     tmark(c, 4, s);
-    launch_combine(c, out, s);
+    launch_combine(c, pl, out, s);
     tmark(c, 5, s);
     c->tev_eval = c->timing;
     const cudaError_t e = cudaGetLastError();

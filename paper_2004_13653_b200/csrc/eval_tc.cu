@@ -1,14 +1,352 @@
-// Step a4: tensor-core Gaussian path (placeholder until the tcgen05 kernel lands).
+// Step a4: tensor-core Gaussian path.
+//
+// Table 1's Gaussian is a product kernel f(s,t) = k(s) k(t), so the block a group
+// of points adds to its window is a genuine dense contraction:
+//     S[row][col] = sum_p ky_p(row) * kx_p(col) = (A . B^T)[row][col],
+//     A[row][p] = ky_p(row) (masked by the point's integer row range),
+//     B[col][p] = kx_p(col) (masked by its column range).
+// A group is a vertical stack of s buckets whose window (B + 2F columns, sB + 2F rows)
+// fills the M = 128 TMEM lanes; N = B + 2F rounded up to 16.
+//
+// One persistent CTA (4 warps) per SM slot pops (group, segment of <= 512 points) items:
+//   * operand generation, all warps: lane = point; for each 8-row (or 8-column) unit the
+//     lane evaluates 8 Gaussian factors by the exact-ratio recurrence (2 SFU + 14 FMUL),
+//     rounds them to fp16 (RN; 10-bit mantissa like tf32) and stores one 16-byte vector
+//     straight into the UMMA operand layout (MN-major, no swizzle: an 8x8 core matrix is
+//     128 contiguous bytes, k-groups 128 B apart (LBO), 8-row groups 512 B apart (SBO));
+//   * one elected thread issues tcgen05.mma.cta_group::1.kind::f16 (M=128, N, K=16) twice
+//     per 32-point chunk, accumulating fp32 in TMEM, and tcgen05.commit's an mbarrier that
+//     frees the operand buffer (double-buffered: generation overlaps the MMAs);
+//   * epilogue: tcgen05.ld (32x32b) of the accumulator, each warp its 32 TMEM lanes, into
+//     the group's splat slot; split groups are summed in segment order by the last
+//     arriving CTA; the combine pass (shared with the direct path) then sums the slots
+//     covering each pixel in a fixed order and applies C/(n h^2).
+#include <cuda_fp16.h>
+
 #include "internal.cuh"
+#include "kernels.cuh"
 
 namespace kde {
 
+constexpr int kTcThreads = 128;
+constexpr int kTcChunk = 32;                  // points per chunk (2 MMAs of K = 16)
+constexpr int kTcABytes = kTcM * kTcChunk * 2;  // 8 KB per A buffer
+constexpr int kMaxStack = 32;
+
+struct TcArgs {
+    Geom g;
+    PathGeom pg;
+    const uint32_t* __restrict__ offsets;
+    const float2* __restrict__ xy;
+    const uint2* __restrict__ rng;
+    const int4* __restrict__ items;
+    const int2* __restrict__ group;
+    int* __restrict__ done;
+    float* __restrict__ splat;
+    int nitems, nslots;
+    int n;          // MMA N
+    int tmem_cols;  // allocated TMEM columns (power of two >= n)
+    float kq, q2;   // Gaussian: -log2(e)/(2 h^2), 2^(2 kq)
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// UMMA shared-memory descriptor: no swizzle, MN-major canonical layout.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+    return d;                // base offset 0, lbo mode 0, layout SWIZZLE_NONE (0)
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int k = 0; k < 16; k++) v[k] = __uint_as_float(r[k]);
+}
+
+__device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
+    const __half2 h = __floats2half2_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// 8 masked Gaussian factors of one point for the unit [c0, c0+8) -> fp16 x 8, stored as one
+// 16-byte vector at the point's slot of the operand core matrix.
+__device__ __forceinline__ void gauss_unit(char* dst, int c0, float ph, int lo, int span, float kq,
+                                           float q2) {
+    const int l0 = max(lo - c0, 0), h0 = min(lo + span - c0, 7);
+    uint4 o = make_uint4(0u, 0u, 0u, 0u);
+    if (l0 <= h0) {
+        const uint32_t m = (2u << h0) - (1u << l0);
+        const float d0 = (float)c0 - ph;
+        float gv = ex2_ftz(d0 * d0 * kq);
+        float r = ex2_ftz(fmaf(2.0f, d0, 1.0f) * kq);
+        float f[8];
+#pragma unroll
+        for (int e = 0; e < 8; e++) {
+            f[e] = (m & (1u << e)) ? gv : 0.f;
+            gv *= r;
+            r *= q2;
+        }
+        o = make_uint4(pack_half2(f[0], f[1]), pack_half2(f[2], f[3]), pack_half2(f[4], f[5]),
+                       pack_half2(f[6], f[7]));
+    }
+    *reinterpret_cast<uint4*>(dst) = o;
+}
+
+__global__ void __launch_bounds__(kTcThreads) tc_splat_kernel(const TcArgs a) {
+    extern __shared__ __align__(1024) char tc_smem[];
+    // [A0 | A1 | B0 | B1] operand buffers, then bookkeeping
+    __shared__ __align__(8) uint64_t s_bar[3];  // operand buffers 0/1 freed; accumulator ready
+    __shared__ uint32_t s_tmem;
+    __shared__ int s_w, s_last;
+    __shared__ uint32_t s_pre[kMaxStack + 1];   // prefix counts of the group's buckets
+    __shared__ uint32_t s_off[kMaxStack];       // first sorted position of each bucket
+
+    const Geom& g = a.g;
+    const PathGeom& pg = a.pg;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const int bbytes = a.n * kTcChunk * 2;
+    char* const abase = tc_smem;                   // A buffer b at abase + b * kTcABytes
+    char* const bbase = tc_smem + 2 * kTcABytes;   // B buffer b at bbase + b * bbytes
+    const uint32_t idesc = (1u << 4)                       // D: f32
+                           | (1u << 15) | (1u << 16)        // A, B: MN-major
+                           | ((uint32_t)(a.n >> 3) << 17)   // N
+                           | ((uint32_t)(kTcM >> 4) << 24); // M = 128
+    const int slot_floats = pg.slot_w * pg.slot_h;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&s_tmem)),
+                     "r"(a.tmem_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (t == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        mbar_init(&s_bar[2], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+    uint32_t nuse[2] = {0u, 0u};  // commits issued per operand buffer (same on all threads)
+    uint32_t nacc = 0;            // accumulator-ready commits
+
+    for (;;) {
+        if (t == 0) s_w = atomicAdd(&a.done[a.nslots], 1);
+        __syncthreads();
+        const int w = s_w;
+        if (w >= a.nitems) break;
+        const int4 it = a.items[w];
+        const int gx = it.x % pg.ngx, gy = it.x / pg.ngx;
+        const int ox = gx * pg.px - g.F, oy = gy * pg.py - g.F;  // window origin (pixels)
+        if (t <= pg.s) {  // bucket prefix counts and starts of this group's stack
+            uint32_t pre = 0;
+            for (int k = 0; k < t; k++) {
+                const int by = gy * pg.s + k;
+                if (by < g.nby) {
+                    const int key = by * g.nbx + gx;
+                    pre += a.offsets[key + 1] - a.offsets[key];
+                }
+            }
+            s_pre[t] = pre;
+            if (t < pg.s) {
+                const int by = gy * pg.s + t;
+                s_off[t] = by < g.nby ? a.offsets[by * g.nbx + gx] : 0u;
+            }
+        }
+        __syncthreads();
+        const int cnt = it.z - it.y;
+        const int nch = (cnt + kTcChunk - 1) / kTcChunk;
+        for (int ch = 0; ch < nch; ch++) {
+            const int b = ch & 1;
+            // the MMAs that last read this buffer must be done
+            if (nuse[b] > 0) mbar_wait(&s_bar[b], (nuse[b] - 1) & 1);
+            // lane's point of this chunk
+            const int q = it.y + ch * kTcChunk + lane;
+            const bool valid = q < it.z;
+            float pxh = 0.f, pyh = 0.f;
+            int ilo = 1 << 29, ispan = 0, jlo = 1 << 29, jspan = 0;
+            if (valid) {
+                int k = 0;
+                while (k + 1 < pg.s && (uint32_t)q >= s_pre[k + 1]) k++;
+                const uint32_t d = s_off[k] + ((uint32_t)q - s_pre[k]);
+                const float2 l = a.xy[d];
+                const uint2 rr = a.rng[d];
+                const int by = gy * pg.s + k;
+                pxh = l.x + (float)(gx * g.B - ox) - 0.5f;  // (c + 1/2) - P = c - (P - 1/2)
+                pyh = l.y + (float)(by * g.B - oy) - 0.5f;
+                ilo = (int)(rr.x & 0xffffu) - ox;
+                ispan = (int)(rr.x >> 16) - (int)(rr.x & 0xffffu);
+                jlo = (int)(rr.y & 0xffffu) - oy;
+                jspan = (int)(rr.y >> 16) - (int)(rr.y & 0xffffu);
+            }
+            // operand core-matrix offset of this lane (point = k index)
+            const int koff = (lane >> 3) * 128 + (lane & 7) * 16;
+            char* const ab = abase + b * kTcABytes;
+            char* const bb = bbase + b * bbytes;
+            for (int u = warp; u < kTcM / 8; u += 4)  // A: 16 row units
+                gauss_unit(ab + u * 512 + koff, u * 8, pyh, jlo, jspan, a.kq, a.q2);
+            for (int u = warp; u < a.n / 8; u += 4)   // B: N/8 column units
+                gauss_unit(bb + u * 512 + koff, u * 8, pxh, ilo, ispan, a.kq, a.q2);
+            fence_async_smem();
+            __syncthreads();
+            if (t == 0) {
+                tc_fence_after();
+#pragma unroll
+                for (int kk = 0; kk < 2; kk++) {
+                    const uint64_t ad = umma_desc(smem_u32(ab) + kk * 256, 128, 512);
+                    const uint64_t bd = umma_desc(smem_u32(bb) + kk * 256, 128, 512);
+                    mma_f16(tmem, ad, bd, idesc, (ch > 0 || kk > 0) ? 1u : 0u);
+                }
+                mma_commit(&s_bar[b]);
+                if (ch == nch - 1) mma_commit(&s_bar[2]);
+            }
+            nuse[b]++;
+        }
+        // accumulator ready -> registers -> splat slot (warp w reads TMEM lanes 32w..32w+31)
+        mbar_wait(&s_bar[2], nacc & 1);
+        nacc++;
+        tc_fence_after();
+        {
+            const int row = warp * 32 + lane;
+            float* dst = a.splat + (size_t)it.w * slot_floats + (size_t)row * pg.slot_w;
+            for (int c0 = 0; c0 < a.n; c0 += 16) {
+                float v[16];
+                tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+#pragma unroll
+                for (int k = 0; k < 16; k += 4)
+                    *reinterpret_cast<float4*>(dst + c0 + k) = make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]);
+            }
+        }
+        tc_fence_before();
+        // split group: the last segment to arrive sums all segments in order into segment 0
+        const int2 gr = a.group[it.x];
+        if (gr.y > 1) {
+            __threadfence();
+            __syncthreads();
+            const int slot0 = gr.x;  // one sub-window per group on this path
+            if (t == 0) s_last = (atomicAdd(&a.done[slot0], 1) == gr.y - 1);
+            __syncthreads();
+            if (s_last) {
+                __threadfence();
+                float* d0 = a.splat + (size_t)slot0 * slot_floats;
+                for (int e = t; e < slot_floats; e += blockDim.x) {
+                    float v = __ldcg(d0 + e);
+                    for (int k = 1; k < gr.y; k++) v += __ldcg(d0 + (size_t)k * slot_floats + e);
+                    d0[e] = v;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tmem_cols));
+    }
+}
+
 int launch_tc(kde_ctx* c, float* out, cudaStream_t s) {
-    (void)c;
-    (void)out;
-    (void)s;
-    set_error("kde_eval: tensor-core path not built yet");
-    return KDE_EUNSUPPORTED;
+    EvalPlan& pl = c->plan[KDE_PATH_TENSOR];
+    if (pl.nitems > 0) {
+        TcArgs a;
+        a.g = c->g;
+        a.pg = pl.pg;
+        a.offsets = c->d_offsets;
+        a.xy = c->pb.xy;
+        a.rng = c->pb.rng;
+        a.items = pl.d_items;
+        a.group = pl.d_group;
+        a.done = pl.d_done;
+        a.splat = pl.d_splat;
+        a.nitems = pl.nitems;
+        a.nslots = pl.nslots;
+        a.n = pl.pg.slot_w;
+        a.tmem_cols = 32;
+        while (a.tmem_cols < a.n) a.tmem_cols <<= 1;
+        a.kq = (float)(-0.5 * 1.4426950408889634074 / (c->hpx * c->hpx));
+        a.q2 = (float)exp2(2.0 * (double)a.kq);
+        const size_t smem = 2 * (size_t)kTcABytes + 2 * (size_t)a.n * kTcChunk * 2 + 1024;
+        if (pl.grid <= 0) {
+            cudaFuncSetAttribute(tc_splat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            int nsm = 148, per = 1;
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->p.device);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tc_splat_kernel, kTcThreads, smem);
+            per = std::min(std::max(per, 1), 512 / a.tmem_cols);  // TMEM columns per SM
+            pl.grid = nsm * per;
+        }
+        cudaMemsetAsync(pl.d_done, 0, sizeof(int) * ((size_t)pl.nslots + 1), s);
+        tmark(c, 3, s);
+        tc_splat_kernel<<<std::min(pl.grid, pl.nitems), kTcThreads, smem, s>>>(a);
+        c->launches += 1;
+    } else {
+        tmark(c, 3, s);
+    }
+    tmark(c, 4, s);
+    launch_combine(c, pl, out, s);
+    tmark(c, 5, s);
+    c->tev_eval = c->timing;
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "tensor-core eval launch");
+    return KDE_OK;
 }
 
 }  // namespace kde

@@ -17,6 +17,7 @@ constexpr int kSegPts = 512;      // split-K: points per splat work item (a cons
                                   // plan is invariant under band sharding);
                                   // also bounds every fp32 running sum to 512 terms (R10)
 constexpr int kCombTile = 32;     // combine-pass output tile edge
+constexpr int kTcM = 128;         // tensor-core tile rows = TMEM lanes
 
 // Geometry shared by every kernel (passed by value).
 struct Geom {
@@ -47,27 +48,42 @@ struct PointBufs {
     uint32_t *perm = nullptr;                  // sorted -> original index (alias)
 };
 
+// Geometry of one evaluation path's work decomposition.  A group is a vertical stack of
+// `s` buckets (pitch px x py = B x sB pixels); its window is (px + 2F) x (py + 2F) pixels,
+// cut into nsubx x nsuby sub-windows of sx x sy; each (group, segment, sub-window) block
+// lands in a slot of slot_h rows x slot_w floats.
+struct PathGeom {
+    int s = 1;
+    int ngx = 0, ngy = 0;
+    int px = 0, py = 0;
+    int ww = 0, wh = 0;
+    int nsubx = 1, nsuby = 1;
+    int sx = 0, sy = 0;
+    int slot_w = 0, slot_h = 0;
+    __host__ __device__ int nsub() const { return nsubx * nsuby; }
+    __host__ __device__ int ngroups() const { return ngx * ngy; }
+    __host__ __device__ int64_t slot_floats() const { return (int64_t)slot_w * slot_h; }
+};
+
 struct EvalPlan {
-    // geometry of the splat pass (fixed at create)
-    int nsubx = 1;                             // sub-windows per window side
-    int S = 1;                                 // sub-window edge (pixels)
-    int mt = 4;                                // splat register micro-tile edge
-    int slot_ld = 4;                           // splat slot edge: ceil(S/mt)*mt
+    PathGeom pg;
+    bool enabled = false;
+    // SIMT splat launch shape (direct path)
+    int mt = 4;                                // register micro-tile edge
     int ld = 8;                                // factor row stride (floats)
-    int threads = 32;                          // splat CTA size
-    int grid = 0;                              // persistent splat grid (0: not yet queried)
-    int grid_mt = 0;
+    int threads = 32;                          // CTA size
+    int grid = 0, grid_key = -1;               // persistent grid (0: not yet queried)
     // per-load totals (read back once)
     int tf = 0, tp = 0, nslots = 0, nitems = 0;
     // device buffers
-    uint32_t *d_full = nullptr, *d_part = nullptr, *d_nseg = nullptr;  // nb + 1 each
+    uint32_t *d_full = nullptr, *d_part = nullptr, *d_nseg = nullptr;  // ngroups + 1 each
     uint32_t* d_scan_tmp = nullptr;
-    int2* d_group = nullptr;                   // per bucket: (slot of segment 0, #segments)
-    int* d_totals = nullptr;                   // TF, TP, nslots, -
-    int4* d_items = nullptr;                   // (bucket, k0, k1, slot)
+    int2* d_group = nullptr;                   // per group: (first segment, #segments)
+    int* d_totals = nullptr;                   // TF, TP, nslots, n_binned
+    int4* d_items = nullptr;                   // (group, k0, k1, slot)
     int64_t items_cap = 0;
     float* d_splat = nullptr;
-    int* d_done = nullptr;                     // per slot: arrivals (segment reduce); [nslots] = queue
+    int* d_done = nullptr;                     // per slot arrivals (segment reduce); [nslots] = queue
     int64_t slots_cap = 0;
 };
 
@@ -91,7 +107,7 @@ struct kde_ctx {
     bool timing = false;                       // record phase events (kde_set_timing)
     cudaEvent_t tev[6] = {};                   // bin0, bin1/plan0, plan1, main0, main1, comb1
     bool tev_load = false, tev_eval = false;
-    kde::EvalPlan plan;
+    kde::EvalPlan plan[2];                     // [KDE_PATH_DIRECT], [KDE_PATH_TENSOR]
 };
 
 namespace kde {
@@ -108,7 +124,8 @@ int bin_points(kde_ctx* c, const double* d_x, const double* d_y, int64_t n);
 int launch_direct(kde_ctx* c, float* out, cudaStream_t s);
 int launch_tc(kde_ctx* c, float* out, cudaStream_t s);
 // planning (plan.cu)
-int plan_device(kde_ctx* c);
-int plan_scatter(kde_ctx* c);
+int plan_device(kde_ctx* c, EvalPlan& pl);
+int plan_scatter(kde_ctx* c, EvalPlan& pl);
+int launch_combine(kde_ctx* c, const EvalPlan& pl, float* out, cudaStream_t s);
 
 }  // namespace kde

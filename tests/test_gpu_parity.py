@@ -184,3 +184,68 @@ def test_error_paths_on_device():
     with pytest.raises(KdeError) as e:
         k.eval("tensor")
     assert e.value.code == _lib.KDE_EUNSUPPORTED
+
+
+# --- tensor-core Gaussian path (a4): 2e-3 * max -----------------------------------------
+def _tc(c, rows=None, cutoff=None):
+    k = _kde(c, kernel=6, rows=rows, cutoff=cutoff)
+    k.load(torch.from_numpy(c["x"]).cuda(), torch.from_numpy(c["y"]).cuda())
+    return k
+
+
+def test_tensor_C1_full_raster():
+    preset, n, W, hpx, _, cut, seed = CONFIGS["C1"]
+    c = case(preset, n, W, hpx, seed=seed)
+    k = _tc(c)
+    gpu = k.eval("tensor").cpu().numpy()
+    ref, _ = oracle.kde_raster(_grid(c, kernel=6), c["x"], c["y"], threads=THREADS)
+    err = _err(gpu, ref)
+    assert err <= TOL_TENSOR, err
+    d = k.eval("direct").cpu().numpy()
+    assert np.abs(gpu - d).max() <= TOL_TENSOR * d.max()  # O11: TC vs direct
+
+
+@pytest.mark.parametrize("cutoff", [4.0, 2.5])
+@pytest.mark.parametrize("hpx", [1.5, 3.0, 6.0])
+def test_tensor_adversarial_ragged(cutoff, hpx):
+    c = adversarial(hpx=hpx)
+    k = _tc(c, cutoff=cutoff)
+    gpu = k.eval("tensor").cpu().numpy()
+    ref, _ = oracle.kde_raster(_grid(c, kernel=6, cutoff=cutoff), c["x"], c["y"], threads=THREADS)
+    assert _err(gpu, ref) <= TOL_TENSOR
+
+
+def test_tensor_hot_pixel_split_and_sharding_bitwise():
+    rng = np.random.default_rng(3)
+    n = 60_000
+    res = 10.0
+    c = dict(x=1e6 + (40.3 + rng.normal(0, 3, n)) * res, y=2e6 + (61.7 + rng.normal(0, 5, n)) * res,
+             x0=1e6, y0=2e6, res=res, W=90, H=150, h=3.0 * res, kernel=6, cutoff=4.0)
+    full = _tc(c)
+    a = full.eval("tensor").cpu().numpy()
+    ref, _ = oracle.kde_raster(_grid(c), c["x"], c["y"], threads=THREADS)
+    assert _err(a, ref) <= TOL_TENSOR
+    b = full.eval("tensor").cpu().numpy()
+    np.testing.assert_array_equal(a.view(np.uint32), b.view(np.uint32))
+    parts = [_tc(c, rows=r).eval("tensor").cpu().numpy() for r in ((0, 40), (40, 100), (100, 150))]
+    np.testing.assert_array_equal(np.concatenate(parts).view(np.uint32), a.view(np.uint32))
+
+
+def test_tensor_full_size_sampled_C2():
+    preset, n, W, hpx, _, cut, seed = CONFIGS["C2"]
+    c = case(preset, n, W, hpx, seed=seed)
+    k = _tc(c)
+    gpu = k.eval("tensor").cpu().numpy()
+    hx, hy = hottest_bucket_tile(c["x"], c["y"], c["x0"], c["y0"], c["res"], W, W)
+    pi, pj = sample_pixels(W, W, (0, W), gpu=gpu, tiles=[(hx, hy, 64, 64)], n_random=2048, seed=seed)
+    ref, _ = oracle.kde_pixels(_grid(c, kernel=6), c["x"], c["y"], pi, pj, threads=THREADS)
+    assert np.abs(gpu[pj, pi] - ref).max() <= TOL_TENSOR * ref.max()
+
+
+def test_tensor_unsupported_large_support():
+    c = adversarial(hpx=20.0)  # R = 80 px: window > 128 rows
+    k = _tc(c)
+    from paper_2004_13653_b200 import KdeError
+    with pytest.raises(KdeError) as e:
+        k.eval("tensor")
+    assert e.value.code == -4
