@@ -134,7 +134,7 @@ template <int KERN, bool RADIAL, int MT>
 __global__ void __launch_bounds__(256) splat_kernel(const SplatArgs a) {
     constexpr int ST = mt_stride<MT>();
     extern __shared__ __align__(16) float smem[];
-    __shared__ int s_w, s_last;
+    __shared__ int s_w;
     const Geom& g = a.g;
     const int ld = a.ld;
     float* s_fx = smem;                      // [kChunk][ld]
@@ -227,25 +227,6 @@ __global__ void __launch_bounds__(256) splat_kernel(const SplatArgs a) {
 #pragma unroll
                 for (int c = 0; c < MT; c++) sp[r * slot_ld + c] = acc[r][c];
         }
-        // split group: the last segment to arrive sums all segments IN ORDER into
-        // segment 0's slot (deterministic whichever CTA does it)
-        const int2 gr = a.group[key];
-        if (gr.y > 1) {
-            __threadfence();
-            __syncthreads();
-            const int slot0 = gr.x * nsub + sub;
-            if (t == 0) s_last = (atomicAdd(&a.done[slot0], 1) == gr.y - 1);
-            __syncthreads();
-            if (s_last) {
-                __threadfence();
-                float* d0 = a.splat + (size_t)slot0 * slot_floats;
-                for (int e = t; e < slot_floats; e += blockDim.x) {
-                    float v = __ldcg(d0 + e);
-                    for (int k = 1; k < gr.y; k++) v += __ldcg(d0 + (size_t)k * nsub * slot_floats + e);
-                    d0[e] = v;
-                }
-            }
-        }
     }
 }
 
@@ -270,7 +251,8 @@ struct CombineArgs {
 };
 
 __global__ void __launch_bounds__(256) combine_kernel(const CombineArgs a) {
-    __shared__ int4 s_ent[kMaxEnt];
+    __shared__ int4 s_ent[kMaxEnt];  // (slot of segment 0, origin x, origin y, sw | sh << 16)
+    __shared__ int s_nseg[kMaxEnt];
     __shared__ int s_n;
     const Geom& g = a.g;
     const PathGeom& pg = a.pg;
@@ -307,9 +289,11 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineArgs a) {
                 for (int sx = 0; sx < nx; sx++) {
                     const int ssx = sxa + sx, ssy = sya + sy;
                     const int sw = min(pg.sx, pg.ww - ssx * pg.sx), sh = min(pg.sy, pg.wh - ssy * pg.sy);
-                    if (pos < kMaxEnt)
+                    if (pos < kMaxEnt) {
                         s_ent[pos] = make_int4(gr.x * nsub + ssy * pg.nsubx + ssx, wx0 + ssx * pg.sx,
                                                wy0 + ssy * pg.sy, sw | (sh << 16));
+                        s_nseg[pos] = gr.y;
+                    }
                     pos++;
                 }
             n += __shfl_sync(0xffffffffu, incl, 31);
@@ -322,6 +306,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineArgs a) {
     const int jb = Y0 + (threadIdx.x >> 5);
     const int sl = pg.slot_w;
     const size_t sf = (size_t)pg.slot_floats();
+    const size_t seg_stride = (size_t)nsub * sf;  // slot distance between segments
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
     for (int e0 = 0; e0 < n; e0 += kBatch) {
         float v[kBatch][4];
@@ -330,12 +315,28 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineArgs a) {
             const int e = e0 + b;
             const int4 en = e < n ? s_ent[e] : make_int4(0, 0, 0, 0);
             const int li = i - en.y;
-            const bool inx = e < n && (unsigned)li < (unsigned)(en.w & 0xffff);
+            const int sw = en.w & 0xffff, sh = en.w >> 16, nseg = e < n ? s_nseg[e] : 0;
+            const bool inx = e < n && (unsigned)li < (unsigned)sw;
             const float* sp = a.splat + (size_t)en.x * sf + li;
 #pragma unroll
             for (int k = 0; k < 4; k++) {
                 const int lj = jb + 8 * k - en.z;
-                v[b][k] = (inx && (unsigned)lj < (unsigned)(en.w >> 16)) ? sp[(size_t)lj * sl] : 0.f;
+                float x = 0.f;
+                if (inx && (unsigned)lj < (unsigned)sh) {
+                    const float* q = sp + (size_t)lj * sl;
+                    x = q[0];
+                    int sg = 1;
+                    for (; sg + 4 <= nseg; sg += 4) {  // 4 loads in flight, adds in segment order
+                        const float v0 = q[sg * seg_stride], v1 = q[(sg + 1) * seg_stride];
+                        const float v2 = q[(sg + 2) * seg_stride], v3 = q[(sg + 3) * seg_stride];
+                        x += v0;
+                        x += v1;
+                        x += v2;
+                        x += v3;
+                    }
+                    for (; sg < nseg; sg++) x += q[sg * seg_stride];
+                }
+                v[b][k] = x;
             }
         }
 #pragma unroll

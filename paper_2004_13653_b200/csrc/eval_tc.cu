@@ -18,10 +18,12 @@
 //     per 32-point chunk, accumulating fp32 in TMEM, and tcgen05.commit's an mbarrier that
 //     frees the operand buffer (double-buffered: generation overlaps the MMAs);
 //   * epilogue: tcgen05.ld (32x32b) of the accumulator, each warp its 32 TMEM lanes, into
-//     the group's splat slot; split groups are summed in segment order by the last
-//     arriving CTA; the combine pass (shared with the direct path) then sums the slots
-//     covering each pixel in a fixed order and applies C/(n h^2).
+//     the segment's splat slot; the combine pass (shared with the direct path) then sums,
+//     for every pixel, the slots of all groups and segments covering it in a fixed order
+//     and applies C/(n h^2).
 #include <cuda_fp16.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "internal.cuh"
 #include "kernels.cuh"
@@ -124,9 +126,15 @@ __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
     return *reinterpret_cast<const uint32_t*>(&h);
 }
 
+__device__ __forceinline__ void sts128(uint32_t saddr, uint4 v) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(saddr), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+
 // 8 masked Gaussian factors of one point for the unit [c0, c0+8) -> fp16 x 8, stored as one
-// 16-byte vector at the point's slot of the operand core matrix.
-__device__ __forceinline__ void gauss_unit(char* dst, int c0, float ph, int lo, int span, float kq,
+// 16-byte vector at the point's slot of the operand core matrix (shared address dst).
+__device__ __forceinline__ void gauss_unit(uint32_t dst, int c0, float ph, int lo, int span, float kq,
                                            float q2) {
     const int l0 = max(lo - c0, 0), h0 = min(lo + span - c0, 7);
     uint4 o = make_uint4(0u, 0u, 0u, 0u);
@@ -145,15 +153,15 @@ __device__ __forceinline__ void gauss_unit(char* dst, int c0, float ph, int lo, 
         o = make_uint4(pack_half2(f[0], f[1]), pack_half2(f[2], f[3]), pack_half2(f[4], f[5]),
                        pack_half2(f[6], f[7]));
     }
-    *reinterpret_cast<uint4*>(dst) = o;
+    sts128(dst, o);
 }
 
-__global__ void __launch_bounds__(kTcThreads) tc_splat_kernel(const TcArgs a) {
+__global__ void __launch_bounds__(kTcThreads, 1) tc_splat_kernel(const TcArgs a) {
     extern __shared__ __align__(1024) char tc_smem[];
     // [A0 | A1 | B0 | B1] operand buffers, then bookkeeping
     __shared__ __align__(8) uint64_t s_bar[3];  // operand buffers 0/1 freed; accumulator ready
     __shared__ uint32_t s_tmem;
-    __shared__ int s_w, s_last;
+    __shared__ int s_w;
     __shared__ uint32_t s_pre[kMaxStack + 1];   // prefix counts of the group's buckets
     __shared__ uint32_t s_off[kMaxStack];       // first sorted position of each bucket
 
@@ -161,8 +169,6 @@ __global__ void __launch_bounds__(kTcThreads) tc_splat_kernel(const TcArgs a) {
     const PathGeom& pg = a.pg;
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const int bbytes = a.n * kTcChunk * 2;
-    char* const abase = tc_smem;                   // A buffer b at abase + b * kTcABytes
-    char* const bbase = tc_smem + 2 * kTcABytes;   // B buffer b at bbase + b * bbytes
     const uint32_t idesc = (1u << 4)                       // D: f32
                            | (1u << 15) | (1u << 16)        // A, B: MN-major
                            | ((uint32_t)(a.n >> 3) << 17)   // N
@@ -188,71 +194,100 @@ __global__ void __launch_bounds__(kTcThreads) tc_splat_kernel(const TcArgs a) {
     uint32_t nuse[2] = {0u, 0u};  // commits issued per operand buffer (same on all threads)
     uint32_t nacc = 0;            // accumulator-ready commits
 
+    const uint32_t sm_a = smem_u32(tc_smem);                 // A buffer b at sm_a + b * kTcABytes
+    const uint32_t sm_b = sm_a + 2 * kTcABytes;             // B buffer b at sm_b + b * bbytes
+    const uint32_t koff = (uint32_t)((lane >> 3) * 128 + (lane & 7) * 16);  // point = k index
+    const int nbu = a.n / 8;                                // B column units
+    if (t == 0) s_w = atomicAdd(&a.done[a.nslots], 1);
     for (;;) {
-        if (t == 0) s_w = atomicAdd(&a.done[a.nslots], 1);
         __syncthreads();
         const int w = s_w;
         if (w >= a.nitems) break;
         const int4 it = a.items[w];
+        __syncthreads();                                    // everyone has read s_w
+        if (t == 0) s_w = atomicAdd(&a.done[a.nslots], 1);  // pop the next item early
         const int gx = it.x % pg.ngx, gy = it.x / pg.ngx;
         const int ox = gx * pg.px - g.F, oy = gy * pg.py - g.F;  // window origin (pixels)
-        if (t <= pg.s) {  // bucket prefix counts and starts of this group's stack
-            uint32_t pre = 0;
-            for (int k = 0; k < t; k++) {
-                const int by = gy * pg.s + k;
-                if (by < g.nby) {
-                    const int key = by * g.nbx + gx;
-                    pre += a.offsets[key + 1] - a.offsets[key];
-                }
+        if (warp == 0) {  // bucket prefix counts and starts of this group's stack (warp scan)
+            const int by = gy * pg.s + lane;
+            uint32_t st = 0, cn = 0;
+            if (lane < pg.s && by < g.nby) {
+                const int key = by * g.nbx + gx;
+                st = a.offsets[key];
+                cn = a.offsets[key + 1] - st;
             }
-            s_pre[t] = pre;
-            if (t < pg.s) {
-                const int by = gy * pg.s + t;
-                s_off[t] = by < g.nby ? a.offsets[by * g.nbx + gx] : 0u;
+            uint32_t inc = cn;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += v;
             }
+            if (lane < pg.s) {
+                s_pre[lane + 1] = inc;
+                s_off[lane] = st;
+            }
+            if (lane == 0) s_pre[0] = 0;
         }
         __syncthreads();
         const int cnt = it.z - it.y;
         const int nch = (cnt + kTcChunk - 1) / kTcChunk;
+        const float shx = (float)(gx * g.B - ox) - 0.5f;   // (c + 1/2) - P = c - (P - 1/2)
+        // lane's point position, its bucket within the stack (nondecreasing in q), prefetch
+        int q = it.y + lane;
+        int kb = 0;
+        float2 nl = make_float2(0.f, 0.f);
+        uint2 nr = make_uint2(0u, 0u);
+        int nk = 0;
+        if (q < it.z) {
+            while (kb + 1 < pg.s && (uint32_t)q >= s_pre[kb + 1]) kb++;
+            const uint32_t d = s_off[kb] + ((uint32_t)q - s_pre[kb]);
+            nl = a.xy[d];
+            nr = a.rng[d];
+            nk = kb;
+        }
         for (int ch = 0; ch < nch; ch++) {
             const int b = ch & 1;
-            // the MMAs that last read this buffer must be done
-            if (nuse[b] > 0) mbar_wait(&s_bar[b], (nuse[b] - 1) & 1);
-            // lane's point of this chunk
-            const int q = it.y + ch * kTcChunk + lane;
+            const float2 l = nl;
+            const uint2 rr = nr;
+            const int by = gy * pg.s + nk;
             const bool valid = q < it.z;
+            q += kTcChunk;
+            if (q < it.z) {  // prefetch the next chunk's point
+                while (kb + 1 < pg.s && (uint32_t)q >= s_pre[kb + 1]) kb++;
+                const uint32_t d = s_off[kb] + ((uint32_t)q - s_pre[kb]);
+                nl = a.xy[d];
+                nr = a.rng[d];
+                nk = kb;
+            }
             float pxh = 0.f, pyh = 0.f;
             int ilo = 1 << 29, ispan = 0, jlo = 1 << 29, jspan = 0;
             if (valid) {
-                int k = 0;
-                while (k + 1 < pg.s && (uint32_t)q >= s_pre[k + 1]) k++;
-                const uint32_t d = s_off[k] + ((uint32_t)q - s_pre[k]);
-                const float2 l = a.xy[d];
-                const uint2 rr = a.rng[d];
-                const int by = gy * pg.s + k;
-                pxh = l.x + (float)(gx * g.B - ox) - 0.5f;  // (c + 1/2) - P = c - (P - 1/2)
-                pyh = l.y + (float)(by * g.B - oy) - 0.5f;
+                pxh = l.x + shx;
+                pyh = l.y + ((float)(by * g.B - oy) - 0.5f);
                 ilo = (int)(rr.x & 0xffffu) - ox;
                 ispan = (int)(rr.x >> 16) - (int)(rr.x & 0xffffu);
                 jlo = (int)(rr.y & 0xffffu) - oy;
                 jspan = (int)(rr.y >> 16) - (int)(rr.y & 0xffffu);
             }
-            // operand core-matrix offset of this lane (point = k index)
-            const int koff = (lane >> 3) * 128 + (lane & 7) * 16;
-            char* const ab = abase + b * kTcABytes;
-            char* const bb = bbase + b * bbytes;
-            for (int u = warp; u < kTcM / 8; u += 4)  // A: 16 row units
-                gauss_unit(ab + u * 512 + koff, u * 8, pyh, jlo, jspan, a.kq, a.q2);
-            for (int u = warp; u < a.n / 8; u += 4)   // B: N/8 column units
-                gauss_unit(bb + u * 512 + koff, u * 8, pxh, ilo, ispan, a.kq, a.q2);
+            // the MMAs that last read this buffer must be done
+            if (nuse[b] > 0) mbar_wait(&s_bar[b], (nuse[b] - 1) & 1);
+            const uint32_t ab = sm_a + b * kTcABytes + koff;
+            const uint32_t bb = sm_b + b * bbytes + koff;
+#pragma unroll
+            for (int j = 0; j < kTcM / 32; j++) {  // A: 16 row units, 4 per warp
+                const int u = warp + 4 * j;
+                gauss_unit(ab + u * 512, u * 8, pyh, jlo, jspan, a.kq, a.q2);
+            }
+            for (int u = warp; u < nbu; u += 4)    // B: N/8 column units
+                gauss_unit(bb + u * 512, u * 8, pxh, ilo, ispan, a.kq, a.q2);
             fence_async_smem();
             __syncthreads();
             if (t == 0) {
                 tc_fence_after();
 #pragma unroll
                 for (int kk = 0; kk < 2; kk++) {
-                    const uint64_t ad = umma_desc(smem_u32(ab) + kk * 256, 128, 512);
-                    const uint64_t bd = umma_desc(smem_u32(bb) + kk * 256, 128, 512);
+                    const uint64_t ad = umma_desc(sm_a + b * kTcABytes + kk * 256, 128, 512);
+                    const uint64_t bd = umma_desc(sm_b + b * bbytes + kk * 256, 128, 512);
                     mma_f16(tmem, ad, bd, idesc, (ch > 0 || kk > 0) ? 1u : 0u);
                 }
                 mma_commit(&s_bar[b]);
@@ -276,25 +311,6 @@ __global__ void __launch_bounds__(kTcThreads) tc_splat_kernel(const TcArgs a) {
             }
         }
         tc_fence_before();
-        // split group: the last segment to arrive sums all segments in order into segment 0
-        const int2 gr = a.group[it.x];
-        if (gr.y > 1) {
-            __threadfence();
-            __syncthreads();
-            const int slot0 = gr.x;  // one sub-window per group on this path
-            if (t == 0) s_last = (atomicAdd(&a.done[slot0], 1) == gr.y - 1);
-            __syncthreads();
-            if (s_last) {
-                __threadfence();
-                float* d0 = a.splat + (size_t)slot0 * slot_floats;
-                for (int e = t; e < slot_floats; e += blockDim.x) {
-                    float v = __ldcg(d0 + e);
-                    for (int k = 1; k < gr.y; k++) v += __ldcg(d0 + (size_t)k * slot_floats + e);
-                    d0[e] = v;
-                }
-            }
-        }
-        __syncthreads();
     }
     tc_fence_before();
     __syncthreads();
@@ -327,10 +343,19 @@ int launch_tc(kde_ctx* c, float* out, cudaStream_t s) {
         const size_t smem = 2 * (size_t)kTcABytes + 2 * (size_t)a.n * kTcChunk * 2 + 1024;
         if (pl.grid <= 0) {
             cudaFuncSetAttribute(tc_splat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            int nsm = 148, per = 1;
+            int nsm = 148, per = 0;
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->p.device);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tc_splat_kernel, kTcThreads, smem);
-            per = std::min(std::max(per, 1), 512 / a.tmem_cols);  // TMEM columns per SM
+            const cudaError_t oe =
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tc_splat_kernel, kTcThreads, smem);
+            if (getenv("KDE_DEBUG"))
+                fprintf(stderr, "[kde] tc occupancy query: err=%d per=%d smem=%zu\n", (int)oe, per, smem);
+            // (the occupancy API reports 1 CTA/SM for this kernel; size from the real limits:
+            //  shared memory, and TMEM columns below)
+            if (oe != cudaSuccess) cudaGetLastError();
+            per = std::max(per, (int)((200u << 10) / (smem + 2048)));
+            // persistent CTAs hold their TMEM allocation for the whole launch: never
+            // oversubscribe the 512 columns of an SM
+            per = std::max(1, std::min(per, 512 / a.tmem_cols));
             pl.grid = nsm * per;
         }
         cudaMemsetAsync(pl.d_done, 0, sizeof(int) * ((size_t)pl.nslots + 1), s);
