@@ -108,10 +108,9 @@ static void plan_geometry_tc(EvalPlan& pl, const Geom& g, bool gaussian_product)
 static int alloc_plan(EvalPlan& pl) {
     if (!pl.enabled) return KDE_OK;
     const size_t ng = (size_t)pl.pg.ngroups();
-    cudaError_t e = cudaMalloc(&pl.d_full, sizeof(uint32_t) * (ng + 1));
-    if (e == cudaSuccess) e = cudaMalloc(&pl.d_part, sizeof(uint32_t) * (ng + 1));
-    if (e == cudaSuccess) e = cudaMalloc(&pl.d_nseg, sizeof(uint32_t) * (ng + 1));
-    if (e == cudaSuccess) e = cudaMalloc(&pl.d_scan_tmp, sizeof(uint32_t) * ((ng + 1) / 2048 + 2));
+    const size_t nblk = (size_t)plan_nblk(pl.pg);
+    cudaError_t e = cudaMalloc(&pl.d_local, sizeof(uint64_t) * nblk * 1024);
+    if (e == cudaSuccess) e = cudaMalloc(&pl.d_bsum, sizeof(uint64_t) * (nblk + 1));
     if (e == cudaSuccess) e = cudaMalloc(&pl.d_group, sizeof(int2) * (ng > 0 ? ng : 1));
     if (e == cudaSuccess) e = cudaMalloc(&pl.d_totals, sizeof(int) * 4);
     if (e != cudaSuccess) {
@@ -122,18 +121,26 @@ static int alloc_plan(EvalPlan& pl) {
     return KDE_OK;
 }
 
-// after the totals are known: item list + splat capacity, then the item scatter
-static int finish_plan(kde_ctx* c, EvalPlan& pl, const int* tot) {
+// before planning: the item list at its upper bound (full segments + one partial per
+// group), so the plan can write it without a host round trip
+static int reserve_items(EvalPlan& pl, int64_t n) {
+    if (!pl.enabled) return KDE_OK;
+    const int64_t bound = (n / kSegPts + std::min<int64_t>(n, pl.pg.ngroups())) * pl.pg.nsub() + 1;
+    if (bound > pl.items_cap) {
+        if (dalloc((void**)&pl.d_items, sizeof(int4) * bound, "plan items")) return KDE_ENOMEM;
+        pl.items_cap = bound;
+    }
+    return KDE_OK;
+}
+
+// after the totals are known: splat capacity
+static int finish_plan(EvalPlan& pl, const int* tot) {
     if (!pl.enabled) return KDE_OK;
     const int nsub = pl.pg.nsub();
     pl.tf = tot[0];
     pl.tp = tot[1];
     pl.nslots = tot[2];
     pl.nitems = (pl.tf + pl.tp) * nsub;
-    if (pl.nitems > pl.items_cap) {
-        if (dalloc((void**)&pl.d_items, sizeof(int4) * pl.nitems, "plan items")) return KDE_ENOMEM;
-        pl.items_cap = pl.nitems;
-    }
     if (pl.nslots > pl.slots_cap) {
         if (dalloc((void**)&pl.d_splat, sizeof(float) * (size_t)pl.nslots * pl.pg.slot_floats(),
                    "splat blocks"))
@@ -142,14 +149,12 @@ static int finish_plan(kde_ctx* c, EvalPlan& pl, const int* tot) {
             return KDE_ENOMEM;
         pl.slots_cap = pl.nslots;
     }
-    return plan_scatter(c, pl);
+    return KDE_OK;
 }
 
 static void free_plan(EvalPlan& pl) {
-    cudaFree(pl.d_full);
-    cudaFree(pl.d_part);
-    cudaFree(pl.d_nseg);
-    cudaFree(pl.d_scan_tmp);
+    cudaFree(pl.d_local);
+    cudaFree(pl.d_bsum);
     cudaFree(pl.d_group);
     cudaFree(pl.d_totals);
     cudaFree(pl.d_items);
@@ -344,6 +349,7 @@ int kde_load_points(kde_ctx* c, const double* x, const double* y, int64_t n) {
     tmark(c, 1, c->stream);
     for (int p = 0; p < 2; p++)
         if (c->plan[p].enabled) {
+            if (reserve_items(c->plan[p], n)) return KDE_ENOMEM;
             rc = plan_device(c, c->plan[p]);
             if (rc) return rc;
         }
@@ -365,7 +371,7 @@ int kde_load_points(kde_ctx* c, const double* x, const double* y, int64_t n) {
     c->stats.useful_pairs = (int64_t)st[2];
     c->stats.n_binned = (int64_t)c->h_totals[3];
     for (int p = 0; p < 2; p++) {
-        rc = finish_plan(c, c->plan[p], c->h_totals + 4 * p);
+        rc = finish_plan(c->plan[p], c->h_totals + 4 * p);
         if (rc) return rc;
     }
     e = cudaEventRecord(c->loaded_ev, c->stream);

@@ -101,40 +101,48 @@ __global__ void __launch_bounds__(256) bin_convert_kernel(const double* __restri
 }
 
 // ---------------------------------------------------------------------------------
-// a2: stable LSD counting sort, 8-bit digits (ceil(bits/8) passes), per-block digit
-// histograms -> exclusive scan (digit-major) -> stable in-block ranking + scatter.
+// a2: stable LSD counting sort.  Keys lie in [0, nb] (nb = dropped); passes =
+// ceil(bits/11) with digits of ceil(bits/passes) <= 11 bits (two passes up to 2^22
+// buckets).  Per pass: per-block digit histograms -> exclusive scan (digit-major) ->
+// stable in-block ranking (warp match_any; per-warp digit counts; leaders only clear what
+// they set) + scatter.
 constexpr int kRsThreads = 256;
 constexpr int kRsRounds = 8;
 constexpr int kRsChunk = kRsThreads * kRsRounds;
+constexpr int kRsMaxBits = 11;
 
 __global__ void __launch_bounds__(kRsThreads) rs_upsweep(const uint32_t* __restrict__ keys, int n,
-                                                         int shift, uint32_t* __restrict__ hist,
-                                                         int nblk) {
-    __shared__ uint32_t h[256];
-    h[threadIdx.x] = 0;
+                                                         int shift, uint32_t dmask,
+                                                         uint32_t* __restrict__ hist, int nblk) {
+    extern __shared__ uint32_t h[];  // [dmask + 1]
+    const int nbins = (int)dmask + 1;
+    for (int d = threadIdx.x; d < nbins; d += kRsThreads) h[d] = 0;
     __syncthreads();
     const int base = blockIdx.x * kRsChunk;
 #pragma unroll
     for (int r = 0; r < kRsRounds; r++) {
         const int i = base + r * kRsThreads + threadIdx.x;
-        if (i < n) atomicAdd(&h[(keys[i] >> shift) & 255u], 1u);
+        if (i < n) atomicAdd(&h[(keys[i] >> shift) & dmask], 1u);
     }
     __syncthreads();
-    hist[(size_t)threadIdx.x * nblk + blockIdx.x] = h[threadIdx.x];
+    for (int d = threadIdx.x; d < nbins; d += kRsThreads) hist[(size_t)d * nblk + blockIdx.x] = h[d];
 }
 
 __global__ void __launch_bounds__(kRsThreads) rs_downsweep(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
-    uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, int n, int shift,
+    uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, int n, int shift, uint32_t dmask,
     const uint32_t* __restrict__ hscan, int nblk) {
-    __shared__ uint32_t run[256];
-    __shared__ uint32_t boff[256];
-    __shared__ uint32_t wcnt[kRsThreads / 32][256];
+    extern __shared__ uint32_t sm[];
+    const int nbins = (int)dmask + 1;
+    uint32_t* run = sm;                                   // [nbins] running count per digit
+    uint32_t* boff = sm + nbins;                          // [nbins] block base per digit
+    uint16_t* wcnt = reinterpret_cast<uint16_t*>(sm + 2 * nbins);  // [8][nbins]
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-    run[t] = 0;
-    boff[t] = hscan[(size_t)t * nblk + blockIdx.x];
-#pragma unroll
-    for (int w = 0; w < kRsThreads / 32; w++) wcnt[w][t] = 0;
+    for (int d = t; d < nbins; d += kRsThreads) {
+        run[d] = 0;
+        boff[d] = hscan[(size_t)d * nblk + blockIdx.x];
+    }
+    for (int e = t; e < (kRsThreads / 32) * nbins; e += kRsThreads) wcnt[e] = 0;
     __syncthreads();
     const uint32_t lt = (1u << lane) - 1u;
     const int base = blockIdx.x * kRsChunk;
@@ -143,26 +151,24 @@ __global__ void __launch_bounds__(kRsThreads) rs_downsweep(
         const bool valid = i < n;
         const uint32_t k = valid ? kin[i] : 0u;
         const uint32_t v = valid ? (vin ? vin[i] : (uint32_t)i) : 0u;
-        const uint32_t d = valid ? ((k >> shift) & 255u) : (0x1000u + lane);  // unique if invalid
+        const uint32_t d = valid ? ((k >> shift) & dmask) : (0x10000u + lane);  // unique if invalid
         const uint32_t peers = __match_any_sync(0xffffffffu, d);
         const uint32_t lrank = __popc(peers & lt);
-        if (valid && lrank == 0) wcnt[warp][d] = __popc(peers);
+        const bool leader = valid && lrank == 0;
+        if (leader) wcnt[warp * nbins + d] = (uint16_t)__popc(peers);
         __syncthreads();
         if (valid) {
             uint32_t pos = run[d] + lrank;
-            for (int w = 0; w < warp; w++) pos += wcnt[w][d];
+            for (int w = 0; w < warp; w++) pos += wcnt[w * nbins + d];
             const uint32_t dst = boff[d] + pos;
             kout[dst] = k;
             vout[dst] = v;
         }
         __syncthreads();
-        uint32_t s = 0;
-#pragma unroll
-        for (int w = 0; w < kRsThreads / 32; w++) {
-            s += wcnt[w][t];
-            wcnt[w][t] = 0;
+        if (leader) {
+            atomicAdd(&run[d], (uint32_t)__popc(peers));
+            wcnt[warp * nbins + d] = 0;
         }
-        run[t] += s;
         __syncthreads();
     }
 }
@@ -317,7 +323,7 @@ int bin_points(kde_ctx* c, const double* d_x, const double* d_y, int64_t n64) {
         if (rc) return KDE_ENOMEM;
         pb.cap = cap;
     }
-    const int64_t hneed = (int64_t)256 * (nblk > 0 ? nblk : 1);
+    const int64_t hneed = (int64_t)2048 * (nblk > 0 ? nblk : 1);
     if (hneed > pb.hist_cap) {
         if (grow((void**)&pb.hist, sizeof(uint32_t) * hneed)) return KDE_ENOMEM;
         if (grow((void**)&pb.scan_tmp, sizeof(uint32_t) * (hneed / kScanChunk + 2))) return KDE_ENOMEM;
@@ -331,15 +337,25 @@ int bin_points(kde_ctx* c, const double* d_x, const double* d_y, int64_t n64) {
         // LSD passes over the key bits of [0, nb]
         int bits = 1;
         while ((1ull << bits) <= nb) bits++;
-        const int passes = (bits + 7) / 8;
+        const int passes = (bits + kRsMaxBits - 1) / kRsMaxBits;
+        const int dbits = (bits + passes - 1) / passes;
+        const uint32_t dmask = (1u << dbits) - 1u;
+        const size_t up_smem = sizeof(uint32_t) * (dmask + 1);
+        const size_t dn_smem = sizeof(uint32_t) * 2 * (dmask + 1) + sizeof(uint16_t) * 8 * (dmask + 1);
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(rs_downsweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(sizeof(uint32_t) * 2 * 2048 + sizeof(uint16_t) * 8 * 2048));
+            attr = true;
+        }
         int cur = 0;
         for (int ps = 0; ps < passes; ps++) {
-            const int shift = ps * 8;
-            rs_upsweep<<<nblk, kRsThreads, 0, s>>>(pb.key[cur], n, shift, pb.hist, nblk);
-            c->launches += 2 + scan_excl_u32(pb.hist, (int64_t)256 * nblk, pb.scan_tmp, s);
-            rs_downsweep<<<nblk, kRsThreads, 0, s>>>(pb.key[cur], ps == 0 ? nullptr : pb.val[cur],
-                                                     pb.key[cur ^ 1], pb.val[cur ^ 1], n, shift,
-                                                     pb.hist, nblk);
+            const int shift = ps * dbits;
+            rs_upsweep<<<nblk, kRsThreads, up_smem, s>>>(pb.key[cur], n, shift, dmask, pb.hist, nblk);
+            c->launches += 2 + scan_excl_u32(pb.hist, (int64_t)(dmask + 1) * nblk, pb.scan_tmp, s);
+            rs_downsweep<<<nblk, kRsThreads, dn_smem, s>>>(pb.key[cur], ps == 0 ? nullptr : pb.val[cur],
+                                                          pb.key[cur ^ 1], pb.val[cur ^ 1], n, shift,
+                                                          dmask, pb.hist, nblk);
             cur ^= 1;
         }
         pb.perm = pb.val[cur];

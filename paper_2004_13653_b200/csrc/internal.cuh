@@ -76,8 +76,8 @@ struct EvalPlan {
     // per-load totals (read back once)
     int tf = 0, tp = 0, nslots = 0, nitems = 0;
     // device buffers
-    uint32_t *d_full = nullptr, *d_part = nullptr, *d_nseg = nullptr;  // ngroups + 1 each
-    uint32_t* d_scan_tmp = nullptr;
+    uint64_t* d_local = nullptr;               // block-local prefixes (full << 32 | part)
+    uint64_t* d_bsum = nullptr;                // block totals -> their exclusive scan
     int2* d_group = nullptr;                   // per group: (first segment, #segments)
     int* d_totals = nullptr;                   // TF, TP, nslots, n_binned
     int4* d_items = nullptr;                   // (group, k0, k1, slot)
@@ -125,7 +125,7 @@ int launch_direct(kde_ctx* c, float* out, cudaStream_t s);
 int launch_tc(kde_ctx* c, float* out, cudaStream_t s);
 // planning (plan.cu)
 int plan_device(kde_ctx* c, EvalPlan& pl);
-int plan_scatter(kde_ctx* c, EvalPlan& pl);
+int plan_nblk(const PathGeom& pg);
 int launch_combine(kde_ctx* c, const EvalPlan& pl, float* out, cudaStream_t s);
 
 }  // namespace kde

@@ -1,14 +1,15 @@
-// Device-side evaluation plan: from the bucket offsets, with no host
-// round trip except one 16-byte read of the totals.  One plan per evaluation path; a
-// path's group is a vertical stack of pg.s buckets (1 for the direct path).
+// Device-side evaluation plan, three kernels per path and no host round
+// trip except one 16-byte read of the totals (for the splat-buffer capacity).  A path's
+// group is a vertical stack of pg.s buckets (1 for the direct path).
 //
-//   plan_count    per group g whose window meets the band: cnt_g = sum of its buckets'
-//                 counts; full_g = cnt_g / kSegPts segments, part_g = [cnt_g % kSegPts != 0]
-//   3 scans       exclusive scans of full_g, part_g, nseg_g = full_g + part_g
-//   plan_finish   group[g] = (first segment, nseg_g) and the totals (TF, TP, nslots, binned)
-//   plan_scatter  the item list: all full segments first (equal work), then the partial
-//                 ones; item = (g, k0, k1, slot), slot = (seg_scan_g + seg)*nsub + sub, where
-//                 [k0, k1) are positions in the concatenation of the group's bucket ranges
+//   plan_local    per group g whose window meets the band: cnt_g = sum of its buckets'
+//                 counts, full_g = cnt_g / kSegPts full segments, part_g = [cnt_g % kSegPts];
+//                 block-local exclusive scan of the packed pair (full_g << 32 | part_g)
+//   plan_blocks   one CTA: exclusive scan of the block totals
+//   plan_finish   global prefixes -> group[g] = (first segment, #segments), the item list
+//                 (all full segments first -- equal work -- then the partial ones;
+//                 item = (g, k0, k1, slot), slot = (first segment + seg)*nsub + sub, [k0, k1)
+//                 positions in the concatenation of the group's bucket ranges) and totals
 //
 // The plan depends only on each group's own counts, so a banded context plans every group
 // it shares with the unbanded one identically (bitwise sharding).
@@ -16,7 +17,9 @@
 
 namespace kde {
 
-int scan_excl_u32(uint32_t* a, int64_t L, uint32_t* tmp, cudaStream_t s);  // bin.cu
+constexpr int kPlanThreads = 256;
+constexpr int kPlanPer = 4;  // groups per thread
+constexpr int kPlanTile = kPlanThreads * kPlanPer;
 
 __device__ __forceinline__ uint32_t group_count(const Geom& g, const PathGeom& pg,
                                                 const uint32_t* __restrict__ off, int gx, int gy) {
@@ -30,101 +33,132 @@ __device__ __forceinline__ uint32_t group_count(const Geom& g, const PathGeom& p
     return c;
 }
 
-__global__ void plan_count_kernel(const Geom g, const PathGeom pg, const uint32_t* __restrict__ off,
-                                  uint32_t* __restrict__ full, uint32_t* __restrict__ part,
-                                  uint32_t* __restrict__ nseg) {
-    const int ng = pg.ngroups();
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= ng; i += gridDim.x * blockDim.x) {
-        uint32_t f = 0, p = 0;
-        if (i < ng) {
-            const int gx = i % pg.ngx, gy = i / pg.ngx;
-            const int wy0 = gy * pg.py - g.F, wy1 = wy0 + pg.wh - 1;
-            if (wy1 >= g.rb && wy0 <= g.re - 1) {  // window meets the band
-                const uint32_t cnt = group_count(g, pg, off, gx, gy);
-                f = cnt / kSegPts;
-                p = (cnt % kSegPts) ? 1u : 0u;
-            }
-        }
-        full[i] = f;  // entry ng stays 0: the exclusive scan then ends with the total
-        part[i] = p;
-        nseg[i] = f + p;
-    }
+__device__ __forceinline__ uint64_t group_pair(const Geom& g, const PathGeom& pg,
+                                               const uint32_t* __restrict__ off, int i, uint32_t* cnt) {
+    *cnt = 0;
+    if (i >= pg.ngroups()) return 0;
+    const int gx = i % pg.ngx, gy = i / pg.ngx;
+    const int wy0 = gy * pg.py - g.F, wy1 = wy0 + pg.wh - 1;
+    if (wy1 < g.rb || wy0 > g.re - 1) return 0;  // window misses the band
+    const uint32_t c = group_count(g, pg, off, gx, gy);
+    *cnt = c;
+    return ((uint64_t)(c / kSegPts) << 32) | (uint64_t)((c % kSegPts) ? 1u : 0u);
 }
 
-__global__ void plan_finish_kernel(const uint32_t* __restrict__ off, int nb,
-                                   const uint32_t* __restrict__ full_s,
-                                   const uint32_t* __restrict__ part_s,
-                                   const uint32_t* __restrict__ nseg_s, int ng, int nsub,
-                                   int2* __restrict__ group, int* __restrict__ totals) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ng; i += gridDim.x * blockDim.x)
-        group[i] = make_int2((int)nseg_s[i], (int)(nseg_s[i + 1] - nseg_s[i]));
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        totals[0] = (int)full_s[ng];            // full segments
-        totals[1] = (int)part_s[ng];            // partial segments
-        totals[2] = (int)nseg_s[ng] * nsub;     // slots
-        totals[3] = (int)off[nb];               // points binned
+// block-wide exclusive scan of one u64 per thread (kPlanThreads threads); returns the total
+__device__ __forceinline__ uint64_t block_scan_u64(uint64_t v, uint64_t* s_warp, uint64_t* total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint64_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t x = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += x;
     }
+    if (lane == 31) s_warp[w] = inc;
+    __syncthreads();
+    uint64_t pre = 0, tot = 0;
+    for (int k = 0; k < kPlanThreads / 32; k++) {
+        pre += (k < w) ? s_warp[k] : 0;
+        tot += s_warp[k];
+    }
+    *total = tot;
+    return pre + inc - v;
 }
 
-// one thread per group: write its items (full segments into [0, TF*nsub), the partial one
-// into [TF*nsub, (TF+TP)*nsub)), sub-window index fastest
-__global__ void plan_scatter_kernel(const Geom g, const PathGeom pg, const uint32_t* __restrict__ off,
-                                    const uint32_t* __restrict__ full_s,
-                                    const uint32_t* __restrict__ part_s,
-                                    const uint32_t* __restrict__ nseg_s, int TF,
-                                    int4* __restrict__ items) {
-    const int ng = pg.ngroups(), nsub = pg.nsub();
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ng; i += gridDim.x * blockDim.x) {
-        const int nf = (int)(full_s[i + 1] - full_s[i]);
-        const int np = (int)(part_s[i + 1] - part_s[i]);
-        if (nf + np == 0) continue;
-        const int cnt = (int)group_count(g, pg, off, i % pg.ngx, i / pg.ngx);
-        const int sb = (int)nseg_s[i];
+__global__ void __launch_bounds__(kPlanThreads) plan_local_kernel(const Geom g, const PathGeom pg,
+                                                                  const uint32_t* __restrict__ off,
+                                                                  uint64_t* __restrict__ local,
+                                                                  uint64_t* __restrict__ bsum) {
+    __shared__ uint64_t s_warp[kPlanThreads / 32];
+    const int i0 = blockIdx.x * kPlanTile + threadIdx.x * kPlanPer;
+    uint64_t v[kPlanPer], sum = 0;
+    uint32_t c;
+#pragma unroll
+    for (int k = 0; k < kPlanPer; k++) {
+        v[k] = group_pair(g, pg, off, i0 + k, &c);
+        sum += v[k];
+    }
+    uint64_t tot;
+    uint64_t run = block_scan_u64(sum, s_warp, &tot);
+#pragma unroll
+    for (int k = 0; k < kPlanPer; k++) {
+        if (i0 + k <= pg.ngroups()) local[i0 + k] = run;
+        run += v[k];
+    }
+    if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+// one CTA: exclusive scan of the block totals, in place; bsum[nblk] = grand total
+__global__ void __launch_bounds__(kPlanThreads) plan_blocks_kernel(uint64_t* __restrict__ bsum, int nblk) {
+    __shared__ uint64_t s_warp[kPlanThreads / 32];
+    __shared__ uint64_t s_carry;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (int b0 = 0; b0 < nblk; b0 += kPlanThreads) {
+        const int b = b0 + threadIdx.x;
+        const uint64_t v = b < nblk ? bsum[b] : 0;
+        uint64_t tot;
+        const uint64_t ex = block_scan_u64(v, s_warp, &tot);
+        const uint64_t carry = s_carry;
+        if (b < nblk) bsum[b] = carry + ex;
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry = carry + tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) bsum[nblk] = s_carry;
+}
+
+__global__ void __launch_bounds__(kPlanThreads) plan_finish_kernel(
+    const Geom g, const PathGeom pg, const uint32_t* __restrict__ off, const uint64_t* __restrict__ local,
+    const uint64_t* __restrict__ bsum, int nblk, int2* __restrict__ group, int4* __restrict__ items,
+    int* __restrict__ totals) {
+    const uint64_t T = bsum[nblk];
+    const int TF = (int)(T >> 32), TP = (int)(T & 0xffffffffu);
+    const int nsub = pg.nsub(), ng = pg.ngroups();
+    const int i0 = blockIdx.x * kPlanTile + threadIdx.x * kPlanPer;
+    const uint64_t base = bsum[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < kPlanPer; k++) {
+        const int i = i0 + k;
+        if (i >= ng) break;
+        const uint64_t pre = base + local[i];
+        uint32_t cnt;
+        const uint64_t own = group_pair(g, pg, off, i, &cnt);
+        const int fs = (int)(pre >> 32), ps = (int)(pre & 0xffffffffu);
+        const int nf = (int)(own >> 32), np = (int)(own & 0xffffffffu);
+        const int sb = fs + ps;  // first segment (segments numbered group by group)
+        group[i] = make_int2(sb, nf + np);
         for (int sg = 0; sg < nf; sg++)
             for (int sub = 0; sub < nsub; sub++)
-                items[((int)full_s[i] + sg) * nsub + sub] =
+                items[(fs + sg) * nsub + sub] =
                     make_int4(i, sg * kSegPts, (sg + 1) * kSegPts, (sb + sg) * nsub + sub);
         if (np)
             for (int sub = 0; sub < nsub; sub++)
-                items[(TF + (int)part_s[i]) * nsub + sub] =
-                    make_int4(i, nf * kSegPts, cnt, (sb + nf) * nsub + sub);
+                items[(TF + ps) * nsub + sub] = make_int4(i, nf * kSegPts, (int)cnt, (sb + nf) * nsub + sub);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        totals[0] = TF;                 // full segments
+        totals[1] = TP;                 // partial segments
+        totals[2] = (TF + TP) * nsub;   // slots
+        totals[3] = (int)off[g.nbx * g.nby];  // points binned
     }
 }
 
-static int grid_for(int64_t n) {
-    const int64_t g = (n + 255) / 256;
-    return (int)(g < 148 * 16 ? (g > 0 ? g : 1) : 148 * 16);
-}
+int plan_nblk(const PathGeom& pg) { return (pg.ngroups() + 1 + kPlanTile - 1) / kPlanTile; }
 
-// Enqueue plan_count, the scans and plan_finish on the context stream; totals land in
-// pl.d_totals (device) -- the caller reads them back.
+// Enqueue the three plan kernels of one path on the context stream; the item list must
+// already have its upper-bound capacity; totals land in pl.d_totals.
 int plan_device(kde_ctx* c, EvalPlan& pl) {
-    const Geom& g = c->g;
     const PathGeom& pg = pl.pg;
-    const int ng = pg.ngroups();
+    const int nblk = plan_nblk(pg);
     cudaStream_t s = c->stream;
-    plan_count_kernel<<<grid_for(ng + 1), 256, 0, s>>>(g, pg, c->d_offsets, pl.d_full, pl.d_part,
-                                                       pl.d_nseg);
-    c->launches += 1;
-    c->launches += scan_excl_u32(pl.d_full, ng + 1, pl.d_scan_tmp, s);
-    c->launches += scan_excl_u32(pl.d_part, ng + 1, pl.d_scan_tmp, s);
-    c->launches += scan_excl_u32(pl.d_nseg, ng + 1, pl.d_scan_tmp, s);
-    plan_finish_kernel<<<grid_for(ng), 256, 0, s>>>(c->d_offsets, g.nbx * g.nby, pl.d_full,
-                                                    pl.d_part, pl.d_nseg, ng, pg.nsub(),
-                                                    pl.d_group, pl.d_totals);
-    c->launches += 1;
+    plan_local_kernel<<<nblk, kPlanThreads, 0, s>>>(c->g, pg, c->d_offsets, pl.d_local, pl.d_bsum);
+    plan_blocks_kernel<<<1, kPlanThreads, 0, s>>>(pl.d_bsum, nblk);
+    plan_finish_kernel<<<nblk, kPlanThreads, 0, s>>>(c->g, pg, c->d_offsets, pl.d_local, pl.d_bsum,
+                                                     nblk, pl.d_group, pl.d_items, pl.d_totals);
+    c->launches += 3;
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "plan launch");
-    return KDE_OK;
-}
-
-int plan_scatter(kde_ctx* c, EvalPlan& pl) {
-    const int ng = pl.pg.ngroups();
-    plan_scatter_kernel<<<grid_for(ng), 256, 0, c->stream>>>(c->g, pl.pg, c->d_offsets, pl.d_full,
-                                                            pl.d_part, pl.d_nseg, pl.tf, pl.d_items);
-    c->launches += 1;
-    const cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return cuda_fail(e, "plan scatter launch");
     return KDE_OK;
 }
 
