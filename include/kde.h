@@ -100,13 +100,18 @@ typedef struct {
     int64_t n_finite;      /* finite points = the n of 1/(n h^2)                           */
     int64_t n_binned;      /* points kept for evaluation                                   */
     int64_t n_outside;     /* finite points dropped: window misses the raster, or (banded)
-                              home bucket row outside the band's reach                     */
+                              home bucket row outside [band_lo, band_hi]                   */
     int64_t useful_pairs;  /* sum over kept points of |box window clipped to raster
                               columns x band rows| = (pixel, point) pairs inside the box
                               support; the "kernel evaluations" of the metric              */
     int32_t bucket;        /* bucket edge B in pixels (power of two)                       */
     int32_t nbx, nby;      /* bucket grid ceil(W/B) x ceil(H/B)                            */
     int32_t reach_px;      /* ceil(R + 1/2) + 1: max pixel distance window <- home pixel   */
+    int32_t stack;         /* bucket rows per tensor-core group (1 if that path is off); the
+                              band filter keeps whole stacks                                */
+    int32_t band_lo, band_hi; /* kept home-bucket rows: [floor(l/stack)*stack,
+                              (floor(h/stack)+1)*stack - 1] with l = rb/B - nr,
+                              h = (re-1)/B + nr, nr = ceil(reach_px/B)                      */
     int64_t kernel_launches; /* CUDA kernels this context has launched so far (cumulative)  */
 } kde_stats;
 

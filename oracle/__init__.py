@@ -73,8 +73,8 @@ def lib():
         L.oracle_kde_pixels.argtypes = [P(_Params), dp, dp, ctypes.c_int64, i32p, i32p,
                                         ctypes.c_int64, dp, u8p, ctypes.c_int]
         L.oracle_bin.restype = ctypes.c_int64
-        L.oracle_bin.argtypes = [P(_Params), ctypes.c_int32, dp, dp, ctypes.c_int64, i64p, i64p,
-                                 f32p, f32p, i32p, P(_Stats)]
+        L.oracle_bin.argtypes = [P(_Params), ctypes.c_int32, ctypes.c_int32, dp, dp, ctypes.c_int64,
+                                 i64p, i64p, f32p, f32p, i32p, P(_Stats)]
         L.oracle_ved.restype = ctypes.c_double
         L.oracle_ved.argtypes = [ctypes.c_double] * 6
         L.oracle_dp_compress.restype = ctypes.c_int64
@@ -160,7 +160,7 @@ def kde_raster(g: Grid, x, y, threads: int = 1, want_ties: bool = False):
     return out, res[1]
 
 
-def bin_points(g: Grid, B: int, x, y):
+def bin_points(g: Grid, B: int, x, y, stack: int = 1):
     """Binning oracle (steps a1/a2): stable counting sort of points by home bucket.
 
     Returns dict(offsets int64[nb+1], perm int64[m], lx, ly float32[m],
@@ -178,7 +178,7 @@ def bin_points(g: Grid, B: int, x, y):
     rng = np.zeros((max(n, 1), 4), np.int32)
     st = _Stats()
     c = g._c()
-    m = lib().oracle_bin(ctypes.byref(c), B, _ptr(x, ctypes.c_double), _ptr(y, ctypes.c_double), n,
+    m = lib().oracle_bin(ctypes.byref(c), B, stack, _ptr(x, ctypes.c_double), _ptr(y, ctypes.c_double), n,
                          _ptr(offsets, ctypes.c_int64), _ptr(perm, ctypes.c_int64),
                          _ptr(lx, ctypes.c_float), _ptr(ly, ctypes.c_float),
                          _ptr(rng, ctypes.c_int32), ctypes.byref(st))

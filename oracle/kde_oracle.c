@@ -214,13 +214,16 @@ int32_t oracle_reach_px(const oracle_params *p)
 }
 
 /*
- * Bin n points into B x B pixel buckets.
+ * Bin n points into B x B pixel buckets.  For a band, keep points whose home bucket row is
+ * in [floor(l/stack)*stack, (floor(h/stack)+1)*stack - 1], l = rb/B - nr, h = (re-1)/B + nr.
  *   outputs (caller-allocated, n entries / nb+1 entries):
  *   offsets[nb+1], perm[n], lx[n], ly[n] (float), rng[4n] (i_lo,i_hi,j_lo,j_hi; int32)
  * Returns n_binned.  nb = ceil(W/B) * ceil(H/B).
  */
-int64_t oracle_bin(const oracle_params *p, int32_t B, const double *x, const double *y, int64_t n,
-                   int64_t *offsets, int64_t *perm, float *lx, float *ly, int32_t *rng,
+static int32_t floordiv32(int32_t a, int32_t b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
+int64_t oracle_bin(const oracle_params *p, int32_t B, int32_t stack, const double *x, const double *y,
+                   int64_t n, int64_t *offsets, int64_t *perm, float *lx, float *ly, int32_t *rng,
                    oracle_stats *st)
 {
     int32_t W = p->width, H = p->height;
@@ -231,7 +234,9 @@ int64_t oracle_bin(const oracle_params *p, int32_t B, const double *x, const dou
     double R = oracle_rpx(p);
     int32_t reach = oracle_reach_px(p);
     int32_t nr = (reach + B - 1) / B;                  /* neighbourhood in buckets */
-    int32_t band_lo = rb / B - nr, band_hi = (re - 1) / B + nr;  /* kept bucket rows */
+    /* kept bucket rows: the band's reach, rounded out to whole stacks of `stack` rows */
+    int32_t band_lo = floordiv32(rb / B - nr, stack) * stack;
+    int32_t band_hi = (floordiv32((re - 1) / B + nr, stack) + 1) * stack - 1;
 
     int64_t *key = malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
     int32_t *r4 = malloc(sizeof(int32_t) * 4 * (size_t)(n > 0 ? n : 1));

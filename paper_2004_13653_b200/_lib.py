@@ -42,6 +42,7 @@ class kde_stats(ctypes.Structure):
                 ("n_binned", ctypes.c_int64), ("n_outside", ctypes.c_int64),
                 ("useful_pairs", ctypes.c_int64), ("bucket", ctypes.c_int32),
                 ("nbx", ctypes.c_int32), ("nby", ctypes.c_int32), ("reach_px", ctypes.c_int32),
+                ("stack", ctypes.c_int32), ("band_lo", ctypes.c_int32), ("band_hi", ctypes.c_int32),
                 ("kernel_launches", ctypes.c_int64)]
 
     def as_dict(self):

@@ -266,11 +266,20 @@ int kde_create(const kde_params* p, kde_ctx** out) {
         }
     }
     g.nr = (g.reach + g.B - 1) / g.B;
-    g.band_lo = rb / g.B - g.nr;
-    g.band_hi = (re - 1) / g.B + g.nr;
-    const size_t nb = (size_t)g.nbx * g.nby;
     plan_geometry_direct(c->plan[KDE_PATH_DIRECT], g);
     plan_geometry_tc(c->plan[KDE_PATH_TENSOR], g, kern == KDE_GAUSSIAN && !c->radial);
+    {   // kept home-bucket rows, rounded out to whole tensor-core stacks so that every group
+        // of either path meeting the band is complete (bitwise sharding)
+        const int st = c->plan[KDE_PATH_TENSOR].enabled ? c->plan[KDE_PATH_TENSOR].pg.s : 1;
+        auto fdiv = [](int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); };
+        const int lo = rb / g.B - g.nr, hi = (re - 1) / g.B + g.nr;
+        g.band_lo = fdiv(lo, st) * st;
+        g.band_hi = (fdiv(hi, st) + 1) * st - 1;
+        c->stats.stack = st;
+        c->stats.band_lo = g.band_lo;
+        c->stats.band_hi = g.band_hi;
+    }
+    const size_t nb = (size_t)g.nbx * g.nby;
     // a BLOCKING stream: loads are ordered after work on the legacy default stream
     // (where device-resident inputs are usually produced, e.g. by PyTorch's default stream)
     cudaError_t e = cudaStreamCreate(&c->stream);

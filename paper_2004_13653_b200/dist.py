@@ -36,7 +36,10 @@ def assemble(band, rows, H, W, group=None):
     if band.shape[0] != maxr:
         raise ValueError(f"band buffer must have {maxr} rows (padded), got {band.shape[0]}")
     buf = torch.empty((world * maxr, W), dtype=band.dtype, device=band.device)
-    dist.all_gather_into_tensor(buf, band.contiguous(), group=group)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(buf, band.contiguous(), group=group)
+    else:  # gloo (CPU tests, or several ranks sharing one GPU): list all-gather
+        dist.all_gather(list(buf.chunk(world)), band.contiguous(), group=group)
     out = torch.empty((H, W), dtype=band.dtype, device=band.device)
     for r, (rb, re) in enumerate(rows):
         if re > rb:

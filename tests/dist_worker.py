@@ -1,0 +1,50 @@
+"""torchrun worker for tests/test_dist_gpu.py: row-band sharded KDE on the GPU(s).
+
+Every rank builds a ShardedKDE over the same synthetic points, evaluates its band and
+all-gathers the heatmap; rank 0 compares it with an unsharded KDE, bitwise, and writes
+the verdict to argv[1].  With one GPU both ranks share cuda:0 and the collective runs on
+gloo (NCCL refuses two ranks on one device); on a multi-GPU box use nccl.
+"""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2004_13653_b200 import KDE  # noqa: E402
+from paper_2004_13653_b200.dist import ShardedKDE  # noqa: E402
+from tests.gpu_cases import case  # noqa: E402
+
+
+def main():
+    out_path, backend = sys.argv[1], sys.argv[2]
+    rank = int(os.environ["RANK"])
+    ngpu = torch.cuda.device_count()
+    dev = int(os.environ.get("LOCAL_RANK", "0")) % ngpu
+    torch.cuda.set_device(dev)
+    dist.init_process_group(backend)
+    res = {}
+    for path in ("direct", "tensor"):
+        c = case("estuary", 150_000, 640, 4.0, seed=33, H=600)
+        sk = ShardedKDE(c["x0"], c["y0"], c["res"], c["W"], c["H"], c["h"], device=dev, tile=64)
+        sk.load(torch.from_numpy(c["x"]).cuda(dev), torch.from_numpy(c["y"]).cuda(dev))
+        full = sk.eval(path).cpu().numpy()
+        if rank == 0:
+            ref = KDE(c["x0"], c["y0"], c["res"], c["W"], c["H"], c["h"], device=dev)
+            ref.load(torch.from_numpy(c["x"]).cuda(dev), torch.from_numpy(c["y"]).cuda(dev))
+            r = ref.eval(path).cpu().numpy()
+            res[path] = bool(np.array_equal(full.view(np.uint32), r.view(np.uint32)))
+            res["bands"] = sk.rows
+    if rank == 0:
+        with open(out_path, "w") as f:
+            json.dump(res, f)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

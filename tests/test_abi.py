@@ -32,12 +32,27 @@ def test_library_exports_every_declared_symbol():
     assert set(_lib.EXPORTS) == set(_declared())
 
 
-def test_struct_layout_matches_header():
+def test_struct_layout_matches_header(tmp_path):
+    """ctypes mirrors == the C compiler's layout of include/kde.h (sizes and offsets)."""
+    import subprocess
     from paper_2004_13653_b200 import _lib
-    # kde_params: 3 doubles, 2 int32, double, int32(+pad), double, 3 int32 (+pad) = 72 bytes
-    assert ctypes.sizeof(_lib.kde_params) == 72
-    assert _lib.kde_params.h.offset == 32 and _lib.kde_params.cutoff.offset == 48
-    assert ctypes.sizeof(_lib.kde_stats) == 64
+    fields = {"kde_params": _lib.kde_params, "kde_stats": _lib.kde_stats, "kde_timing": _lib.kde_timing}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "kde.h"', "int main(void){"]
+    for st, cls in fields.items():
+        lines.append(f'printf("{st} %zu\\n", sizeof({st}));')
+        for f, _ in cls._fields_:
+            lines.append(f'printf("{st}.{f} %zu\\n", offsetof({st}, {f}));')
+    lines.append("return 0;}")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    out = dict(l.split() for l in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                 check=True).stdout.split("\n") if l)
+    for st, cls in fields.items():
+        assert int(out[st]) == ctypes.sizeof(cls), st
+        for f, _ in cls._fields_:
+            assert int(out[f"{st}.{f}"]) == getattr(cls, f).offset, (st, f)
 
 
 def _params(**kw):

@@ -60,7 +60,8 @@ def test_binning_bit_exact(name, rows):
     k = _kde(c, rows=rows)
     k.load(torch.from_numpy(c["x"]).cuda(), torch.from_numpy(c["y"]).cuda())
     got = k.bins()
-    want = oracle.bin_points(_grid(c, rows=rows), got["stats"]["bucket"], c["x"], c["y"])
+    want = oracle.bin_points(_grid(c, rows=rows), got["stats"]["bucket"], c["x"], c["y"],
+                             stack=got["stats"]["stack"])
     for f in ("n_in", "n_finite", "n_binned", "n_outside", "useful_pairs"):
         assert got["stats"][f] == want["stats"][f], f
     np.testing.assert_array_equal(got["offsets"], want["offsets"])

@@ -81,6 +81,21 @@ def test_O8_scan_example_spec190():
     np.testing.assert_array_equal(r["perm"], [1, 0, 2])
 
 
+def test_O8_band_filter_stack_rounding():
+    g = _grid(W=64, H=256, hpx=3.0)
+    x, y = _points(g, 3000, 4)
+    full = oracle.bin_points(g, 16, x, y)
+    reach = oracle.reach_px(g)
+    nr = -(-reach // 16)
+    gb = _grid(W=64, H=256, hpx=3.0, rb=100, re=180)
+    b = oracle.bin_points(gb, 16, x, y, stack=4)
+    lo, hi = ((100 // 16 - nr) // 4) * 4, ((179 // 16 + nr) // 4 + 1) * 4 - 1
+    keys = np.repeat(np.arange(len(full["offsets"]) - 1), np.diff(full["offsets"]))
+    sel = (keys // full["nbx"] >= lo) & (keys // full["nbx"] <= hi)
+    np.testing.assert_array_equal(b["perm"], full["perm"][sel])
+    assert lo % 4 == 0 and (hi + 1) % 4 == 0
+
+
 def test_O8_band_filter_keeps_reach_rows_and_counts_band_pairs():
     g = _grid(W=64, H=128, hpx=3.0)
     x, y = _points(g, 4000, 3)
