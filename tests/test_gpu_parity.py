@@ -250,3 +250,58 @@ def test_tensor_unsupported_large_support():
     with pytest.raises(KdeError) as e:
         k.eval("tensor")
     assert e.value.code == -4
+
+
+# --- C3 / C4 at full size, in the bench's configuration, on sampled pixels ------------------
+_BIG = {}
+
+
+def _big(cfg):
+    if cfg not in _BIG:
+        preset, n, W, hpx, _, cut, seed = CONFIGS[cfg]
+        _BIG.clear()
+        _BIG[cfg] = case(preset, n, W, hpx, seed=seed)
+    return _BIG[cfg]
+
+
+def _sampled_check(c, kernel, path, tol, n_random=768, cutoff=None):
+    from paper_2004_13653_b200 import KDE
+    W = c["W"]
+    cut = c.get("cutoff", 4.0) if cutoff is None else cutoff
+    k = KDE(c["x0"], c["y0"], c["res"], W, W, c["h"], kernel=kernel, cutoff=cut)
+    k.load(torch.from_numpy(c["x"]).cuda(), torch.from_numpy(c["y"]).cuda())
+    gpu = k.eval(path).cpu().numpy()
+    hx, hy = hottest_bucket_tile(c["x"], c["y"], c["x0"], c["y0"], c["res"], W, W)
+    pi, pj = sample_pixels(W, W, (0, W), gpu=gpu, tiles=[(hx, hy, 24, 24)], n_random=n_random, seed=7)
+    g = oracle.Grid(c["x0"], c["y0"], c["res"], W, W, c["h"], kernel, cut)
+    ref, nf, ties = oracle.kde_pixels(g, c["x"], c["y"], pi, pj, threads=THREADS, want_ties=True)
+    assert nf == k.stats()["n_finite"]
+    d = np.abs(gpu[pj, pi].astype(np.float64) - ref)
+    if kernel & 0x100:
+        d = np.where(ties.astype(bool), 0.0, d)
+    assert d.max() <= tol * ref.max(), (d.max() / ref.max())
+    assert ref.max() >= 0.5 * gpu.max()
+    return k
+
+
+@pytest.mark.parametrize("kernel", list(range(8)) + [2 | 0x100, 6 | 0x100])
+def test_C3_all_kernels_direct_sampled(kernel):
+    """Chengshan-Jiao-shaped 5M points, 4096^2, h = 8 px: all 8 Table-1 kernels."""
+    _sampled_check(_big("C3"), kernel, "direct", TOL_DIRECT)
+
+
+def test_C3_gaussian_tensor_sampled():
+    _sampled_check(_big("C3"), 6, "tensor", TOL_TENSOR)
+
+
+@pytest.mark.parametrize("eps", [None, 0.5, 1.0, 5.0])
+def test_C4_raw_and_dp_compressed(eps):
+    """Zhoushan-shaped 20M points at 8192^2, raw and Douglas-Peucker-compressed (oracle DP,
+    PAPER.md:116-129) at the Table-4 thresholds; direct and tensor paths."""
+    c = dict(_big("C4"))
+    if eps is not None:
+        keep = oracle.dp_compress(c["x"], c["y"], c["cloud"].traj_offsets, eps).astype(bool)
+        c["x"], c["y"] = c["x"][keep], c["y"][keep]
+        assert 0 < keep.sum() < keep.size
+    _sampled_check(c, 6, "direct", TOL_DIRECT, n_random=384)
+    _sampled_check(c, 6, "tensor", TOL_TENSOR, n_random=384)
