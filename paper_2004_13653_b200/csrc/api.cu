@@ -78,7 +78,7 @@ static void plan_geometry_direct(EvalPlan& pl, const Geom& g) {
         }
     }
     const int nm = (pg.sx + pl.mt - 1) / pl.mt;
-    pg.slot_w = pg.slot_h = nm * pl.mt;
+    pg.slot_w = pg.slot_h = ((nm * pl.mt + 3) / 4) * 4;  // float4-aligned slots
     pl.ld = nm * (pl.mt <= 4 ? 4 : 8) + 4;
     pl.enabled = true;
 }
@@ -112,7 +112,8 @@ static int alloc_plan(EvalPlan& pl) {
     cudaError_t e = cudaMalloc(&pl.d_local, sizeof(uint64_t) * nblk * 1024);
     if (e == cudaSuccess) e = cudaMalloc(&pl.d_bsum, sizeof(uint64_t) * (nblk + 1));
     if (e == cudaSuccess) e = cudaMalloc(&pl.d_group, sizeof(int2) * (ng > 0 ? ng : 1));
-    if (e == cudaSuccess) e = cudaMalloc(&pl.d_totals, sizeof(int) * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&pl.d_totals, sizeof(int) * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&pl.d_hot, sizeof(int) * (ng > 0 ? ng : 1));
     if (e != cudaSuccess) {
         cudaGetLastError();
         set_error("kde_create: plan allocation failed");
@@ -141,6 +142,7 @@ static int finish_plan(EvalPlan& pl, const int* tot) {
     pl.tp = tot[1];
     pl.nslots = tot[2];
     pl.nitems = (pl.tf + pl.tp) * nsub;
+    pl.nhot = tot[4];
     if (pl.nslots > pl.slots_cap) {
         if (dalloc((void**)&pl.d_splat, sizeof(float) * (size_t)pl.nslots * pl.pg.slot_floats(),
                    "splat blocks"))
@@ -157,6 +159,7 @@ static void free_plan(EvalPlan& pl) {
     cudaFree(pl.d_bsum);
     cudaFree(pl.d_group);
     cudaFree(pl.d_totals);
+    cudaFree(pl.d_hot);
     cudaFree(pl.d_items);
     cudaFree(pl.d_splat);
     cudaFree(pl.d_done);
@@ -367,20 +370,20 @@ int kde_load_points(kde_ctx* c, const double* x, const double* y, int64_t n) {
     // one small readback: plan totals of both paths + the integer stats
     for (int p = 0; p < 2; p++)
         if (c->plan[p].enabled)
-            cudaMemcpyAsync(c->h_totals + 4 * p, c->plan[p].d_totals, 4 * sizeof(int),
+            cudaMemcpyAsync(c->h_totals + 8 * p, c->plan[p].d_totals, 5 * sizeof(int),
                             cudaMemcpyDeviceToHost, c->stream);
-    cudaMemcpyAsync(c->h_totals + 8, c->d_stats, 3 * sizeof(unsigned long long),
+    cudaMemcpyAsync(c->h_totals + 16, c->d_stats, 3 * sizeof(unsigned long long),
                     cudaMemcpyDeviceToHost, c->stream);
     cudaError_t e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) return cuda_fail(e, "kde_load_points");
-    const unsigned long long* st = reinterpret_cast<const unsigned long long*>(c->h_totals + 8);
+    const unsigned long long* st = reinterpret_cast<const unsigned long long*>(c->h_totals + 16);
     c->stats.n_in = n;
     c->stats.n_finite = (int64_t)st[0];
     c->stats.n_outside = (int64_t)st[1];
     c->stats.useful_pairs = (int64_t)st[2];
-    c->stats.n_binned = (int64_t)c->h_totals[3];
+    c->stats.n_binned = (int64_t)(c->plan[KDE_PATH_DIRECT].enabled ? c->h_totals[3] : c->h_totals[8 + 3]);
     for (int p = 0; p < 2; p++) {
-        rc = finish_plan(c->plan[p], c->h_totals + 4 * p);
+        rc = finish_plan(c->plan[p], c->h_totals + 8 * p);
         if (rc) return rc;
     }
     e = cudaEventRecord(c->loaded_ev, c->stream);

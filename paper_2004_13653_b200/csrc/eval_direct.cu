@@ -230,6 +230,38 @@ __global__ void __launch_bounds__(256) splat_kernel(const SplatArgs a) {
     }
 }
 
+// Segment reduce: for every split group (listed by the planner) and sub-window, the
+// segment blocks are summed IN SEGMENT ORDER into segment 0's slot.  One CTA per
+// (group x sub-window, 1024-float chunk of the slot); float4, 4 segments in flight.
+__global__ void __launch_bounds__(256) segreduce_kernel(const int* __restrict__ hot,
+                                                        const int2* __restrict__ group, int nsub,
+                                                        int slot_floats, float* __restrict__ splat) {
+    const int gsub = blockIdx.y;
+    const int2 gr = group[hot[gsub / nsub]];
+    const int sub = gsub % nsub;
+    const int e = (blockIdx.x * 256 + threadIdx.x) * 4;
+    if (e >= slot_floats) return;
+    float* d0 = splat + ((size_t)gr.x * nsub + sub) * slot_floats + e;
+    const size_t stride = (size_t)nsub * slot_floats;
+    float4 acc = *reinterpret_cast<const float4*>(d0);
+    int k = 1;
+    for (; k + 4 <= gr.y; k += 4) {
+        const float4 v0 = *reinterpret_cast<const float4*>(d0 + k * stride);
+        const float4 v1 = *reinterpret_cast<const float4*>(d0 + (k + 1) * stride);
+        const float4 v2 = *reinterpret_cast<const float4*>(d0 + (k + 2) * stride);
+        const float4 v3 = *reinterpret_cast<const float4*>(d0 + (k + 3) * stride);
+        acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
+        acc.x += v1.x; acc.y += v1.y; acc.z += v1.z; acc.w += v1.w;
+        acc.x += v2.x; acc.y += v2.y; acc.z += v2.z; acc.w += v2.w;
+        acc.x += v3.x; acc.y += v3.y; acc.z += v3.z; acc.w += v3.w;
+    }
+    for (; k < gr.y; k++) {
+        const float4 v = *reinterpret_cast<const float4*>(d0 + k * stride);
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    *reinterpret_cast<float4*>(d0) = acc;
+}
+
 // Combine pass: out(i,j) = scale * sum, in order, of the splat blocks covering (i,j).
 // Works for any path geometry (groups of pitch px x py, windows ww x wh, sub-windows).
 // One CTA per 32x32 tile.  Warp 0 lists the (slot, sub-window origin, size) entries of the
@@ -252,7 +284,6 @@ struct CombineArgs {
 
 __global__ void __launch_bounds__(256) combine_kernel(const CombineArgs a) {
     __shared__ int4 s_ent[kMaxEnt];  // (slot of segment 0, origin x, origin y, sw | sh << 16)
-    __shared__ int s_nseg[kMaxEnt];
     __shared__ int s_n;
     const Geom& g = a.g;
     const PathGeom& pg = a.pg;
@@ -289,11 +320,9 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineArgs a) {
                 for (int sx = 0; sx < nx; sx++) {
                     const int ssx = sxa + sx, ssy = sya + sy;
                     const int sw = min(pg.sx, pg.ww - ssx * pg.sx), sh = min(pg.sy, pg.wh - ssy * pg.sy);
-                    if (pos < kMaxEnt) {
+                    if (pos < kMaxEnt)
                         s_ent[pos] = make_int4(gr.x * nsub + ssy * pg.nsubx + ssx, wx0 + ssx * pg.sx,
                                                wy0 + ssy * pg.sy, sw | (sh << 16));
-                        s_nseg[pos] = gr.y;
-                    }
                     pos++;
                 }
             n += __shfl_sync(0xffffffffu, incl, 31);
@@ -306,7 +335,6 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineArgs a) {
     const int jb = Y0 + (threadIdx.x >> 5);
     const int sl = pg.slot_w;
     const size_t sf = (size_t)pg.slot_floats();
-    const size_t seg_stride = (size_t)nsub * sf;  // slot distance between segments
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
     for (int e0 = 0; e0 < n; e0 += kBatch) {
         float v[kBatch][4];
@@ -315,27 +343,14 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineArgs a) {
             const int e = e0 + b;
             const int4 en = e < n ? s_ent[e] : make_int4(0, 0, 0, 0);
             const int li = i - en.y;
-            const int sw = en.w & 0xffff, sh = en.w >> 16, nseg = e < n ? s_nseg[e] : 0;
+            const int sw = en.w & 0xffff, sh = en.w >> 16;
             const bool inx = e < n && (unsigned)li < (unsigned)sw;
             const float* sp = a.splat + (size_t)en.x * sf + li;
 #pragma unroll
             for (int k = 0; k < 4; k++) {
                 const int lj = jb + 8 * k - en.z;
                 float x = 0.f;
-                if (inx && (unsigned)lj < (unsigned)sh) {
-                    const float* q = sp + (size_t)lj * sl;
-                    x = q[0];
-                    int sg = 1;
-                    for (; sg + 4 <= nseg; sg += 4) {  // 4 loads in flight, adds in segment order
-                        const float v0 = q[sg * seg_stride], v1 = q[(sg + 1) * seg_stride];
-                        const float v2 = q[(sg + 2) * seg_stride], v3 = q[(sg + 3) * seg_stride];
-                        x += v0;
-                        x += v1;
-                        x += v2;
-                        x += v3;
-                    }
-                    for (; sg < nseg; sg++) x += q[sg * seg_stride];
-                }
+                if (inx && (unsigned)lj < (unsigned)sh) x = sp[(size_t)lj * sl];
                 v[b][k] = x;
             }
         }
@@ -406,6 +421,12 @@ KConst make_kconst(double hpx) {
 
 int launch_combine(kde_ctx* c, const EvalPlan& pl, float* out, cudaStream_t s) {
     const Geom& g = c->g;
+    if (pl.nhot > 0) {  // split groups: sum their segments first (fixed order)
+        const int sf = (int)pl.pg.slot_floats();
+        dim3 grid((sf / 4 + 255) / 256, pl.nhot * pl.pg.nsub());
+        segreduce_kernel<<<grid, 256, 0, s>>>(pl.d_hot, pl.d_group, pl.pg.nsub(), sf, pl.d_splat);
+        c->launches += 1;
+    }
     CombineArgs a;
     a.g = g;
     a.pg = pl.pg;

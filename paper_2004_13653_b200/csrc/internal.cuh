@@ -79,7 +79,9 @@ struct EvalPlan {
     uint64_t* d_local = nullptr;               // block-local prefixes (full << 32 | part)
     uint64_t* d_bsum = nullptr;                // block totals -> their exclusive scan
     int2* d_group = nullptr;                   // per group: (first segment, #segments)
-    int* d_totals = nullptr;                   // TF, TP, nslots, n_binned
+    int* d_totals = nullptr;                   // TF, TP, nslots, n_binned, #hot groups
+    int* d_hot = nullptr;                      // groups with > 1 segment (segment reduce)
+    int nhot = 0;
     int4* d_items = nullptr;                   // (group, k0, k1, slot)
     int64_t items_cap = 0;
     float* d_splat = nullptr;

@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_blocks_kernel(uint64_t* __r
 __global__ void __launch_bounds__(kPlanThreads) plan_finish_kernel(
     const Geom g, const PathGeom pg, const uint32_t* __restrict__ off, const uint64_t* __restrict__ local,
     const uint64_t* __restrict__ bsum, int nblk, int2* __restrict__ group, int4* __restrict__ items,
-    int* __restrict__ totals) {
+    int* __restrict__ totals, int* __restrict__ hot) {
     const uint64_t T = bsum[nblk];
     const int TF = (int)(T >> 32), TP = (int)(T & 0xffffffffu);
     const int nsub = pg.nsub(), ng = pg.ngroups();
@@ -128,6 +128,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_finish_kernel(
         const int nf = (int)(own >> 32), np = (int)(own & 0xffffffffu);
         const int sb = fs + ps;  // first segment (segments numbered group by group)
         group[i] = make_int2(sb, nf + np);
+        if (nf + np > 1) hot[atomicAdd(&totals[4], 1)] = i;  // split group: segment reduce
         for (int sg = 0; sg < nf; sg++)
             for (int sub = 0; sub < nsub; sub++)
                 items[(fs + sg) * nsub + sub] =
@@ -152,10 +153,11 @@ int plan_device(kde_ctx* c, EvalPlan& pl) {
     const PathGeom& pg = pl.pg;
     const int nblk = plan_nblk(pg);
     cudaStream_t s = c->stream;
+    cudaMemsetAsync(pl.d_totals + 4, 0, sizeof(int), s);  // hot-group counter
     plan_local_kernel<<<nblk, kPlanThreads, 0, s>>>(c->g, pg, c->d_offsets, pl.d_local, pl.d_bsum);
     plan_blocks_kernel<<<1, kPlanThreads, 0, s>>>(pl.d_bsum, nblk);
     plan_finish_kernel<<<nblk, kPlanThreads, 0, s>>>(c->g, pg, c->d_offsets, pl.d_local, pl.d_bsum,
-                                                     nblk, pl.d_group, pl.d_items, pl.d_totals);
+                                                     nblk, pl.d_group, pl.d_items, pl.d_totals, pl.d_hot);
     c->launches += 3;
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "plan launch");
