@@ -156,7 +156,7 @@ __device__ __forceinline__ void gauss_unit(uint32_t dst, int c0, float ph, int l
     sts128(dst, o);
 }
 
-__global__ void __launch_bounds__(kTcThreads, 1) tc_splat_kernel(const TcArgs a) {
+__global__ void __launch_bounds__(kTcThreads, 8) tc_splat_kernel(const TcArgs a) {
     extern __shared__ __align__(1024) char tc_smem[];
     // [A0 | A1 | B0 | B1] operand buffers, then bookkeeping
     __shared__ __align__(8) uint64_t s_bar[3];  // operand buffers 0/1 freed; accumulator ready
