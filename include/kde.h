@@ -135,9 +135,12 @@ KDE_API int kde_create(const kde_params* p, kde_ctx** out);
  *   n    [in] >= 0 (0 is legal: kde_eval then writes zeros).
  * Runs a1 (fp64 convert, integer support ranges, bucket keys), a2 (stable LSD
  * counting sort by bucket key, gather to bucket-local fp32 SoA) and the
- * evaluation plan on the context's internal stream, then synchronises it
- * (the plan reads back the bucket offsets).  Non-finite points are dropped
- * and not counted in n.
+ * device-side evaluation plan on the context's internal stream, and returns
+ * once the plan's totals are known (one 40-byte readback).  Ordering: device
+ * inputs are read after all work already queued on the legacy default stream
+ * (PyTorch's default stream); binning starts after the context's previous
+ * kde_eval has finished reading the bins; a host-input upload may overlap that
+ * evaluation.  Non-finite points are dropped and not counted in n.
  * Errors: KDE_EINVAL (NULL ctx, n < 0, NULL x/y with n > 0, mixed host/device),
  *   KDE_ENOMEM, KDE_ECUDA.
  */

@@ -283,10 +283,12 @@ int kde_create(const kde_params* p, kde_ctx** out) {
         c->stats.band_hi = g.band_hi;
     }
     const size_t nb = (size_t)g.nbx * g.nby;
-    // a BLOCKING stream: loads are ordered after work on the legacy default stream
-    // (where device-resident inputs are usually produced, e.g. by PyTorch's default stream)
-    cudaError_t e = cudaStreamCreate(&c->stream);
+    // a non-blocking stream: a host-input upload may overlap the previous evaluation; the
+    // load orders itself explicitly (see kde_load_points)
+    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->loaded_ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->evald_ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->input_ev, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaMallocHost(&c->h_totals, 128);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_offsets, sizeof(uint32_t) * (nb + 1));
     if (e == cudaSuccess) e = cudaMalloc(&c->d_stats, sizeof(unsigned long long) * 4);
@@ -353,8 +355,15 @@ int kde_load_points(kde_ctx* c, const double* x, const double* y, int64_t n) {
             cudaMemcpyAsync(c->pb.y, y, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream);
             dx = c->pb.x;
             dy = c->pb.y;
+        } else {
+            // device inputs: read them after the work already queued on the legacy default
+            // stream (where PyTorch's default stream puts their producers)
+            cudaEventRecord(c->input_ev, cudaStreamLegacy);
+            cudaStreamWaitEvent(c->stream, c->input_ev, 0);
         }
     }
+    // the previous evaluation reads the sorted points and the plan that binning rewrites
+    if (c->evaluated) cudaStreamWaitEvent(c->stream, c->evald_ev, 0);
     tmark(c, 0, c->stream);
     int rc = bin_points(c, dx, dy, n);
     if (rc) return rc;
@@ -415,9 +424,14 @@ int kde_eval(kde_ctx* c, int32_t path, float* out, void* stream) {
     cudaError_t e = cudaGetLastError();  // surface earlier asynchronous faults
     if (e != cudaSuccess) return cuda_fail(e, "kde_eval: earlier asynchronous error");
     cudaStream_t s = (cudaStream_t)stream;
-    e = cudaStreamWaitEvent(s, c->loaded_ev, 0);  // the plan scatter of the last load
+    e = cudaStreamWaitEvent(s, c->loaded_ev, 0);  // the plan of the last load
     if (e != cudaSuccess) return cuda_fail(e, "kde_eval: wait for load");
-    return path == KDE_PATH_DIRECT ? launch_direct(c, out, s) : launch_tc(c, out, s);
+    const int rc = path == KDE_PATH_DIRECT ? launch_direct(c, out, s) : launch_tc(c, out, s);
+    if (rc == KDE_OK) {
+        cudaEventRecord(c->evald_ev, s);
+        c->evaluated = true;
+    }
+    return rc;
 }
 
 int kde_set_timing(kde_ctx* c, int enable) {
@@ -540,6 +554,8 @@ void kde_free(kde_ctx* c) {
     free_plan(c->plan[1]);
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->loaded_ev) cudaEventDestroy(c->loaded_ev);
+    if (c->evald_ev) cudaEventDestroy(c->evald_ev);
+    if (c->input_ev) cudaEventDestroy(c->input_ev);
     for (int k = 0; k < 6; k++)
         if (c->tev[k]) cudaEventDestroy(c->tev[k]);
     if (c->h_totals) cudaFreeHost(c->h_totals);

@@ -71,15 +71,29 @@ __global__ void __launch_bounds__(256) bin_convert_kernel(const double* __restri
                                                           unsigned long long* __restrict__ stats) {
     unsigned long long nf = 0, no = 0, up = 0;
     const int rb = g.rb, re = g.re;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const Binned b = bin_point(x[i], y[i], g, sentinel);
-        key[i] = b.key;
-        nf += b.status > 0;
-        no += b.status == 1;
-        if (b.status == 2) {
-            const int jl = max(b.jlo, rb), jh = min(b.jhi, re - 1);
-            if (jh >= jl)
-                up += (unsigned long long)(b.ihi - b.ilo + 1) * (unsigned long long)(jh - jl + 1);
+    constexpr int U = 4;  // points per thread per iteration: loads issued before use
+    const int tile = blockDim.x * U;
+    for (int i0 = blockIdx.x * tile + threadIdx.x; i0 < n; i0 += gridDim.x * tile) {
+        double xv[U], yv[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int i = i0 + u * blockDim.x;
+            xv[u] = i < n ? x[i] : 0.0;
+            yv[u] = i < n ? y[i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int i = i0 + u * blockDim.x;
+            if (i >= n) break;
+            const Binned b = bin_point(xv[u], yv[u], g, sentinel);
+            key[i] = b.key;
+            nf += b.status > 0;
+            no += b.status == 1;
+            if (b.status == 2) {
+                const int jl = max(b.jlo, rb), jh = min(b.jhi, re - 1);
+                if (jh >= jl)
+                    up += (unsigned long long)(b.ihi - b.ilo + 1) * (unsigned long long)(jh - jl + 1);
+            }
         }
     }
     __shared__ unsigned long long s[3][8];
@@ -274,12 +288,31 @@ __global__ void __launch_bounds__(256) gather_kernel(const double* __restrict__ 
                                                      float2* __restrict__ xy,
                                                      uint2* __restrict__ rng) {
     const int nbin = (int)offsets[nb];
-    for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < nbin; d += gridDim.x * blockDim.x) {
-        const uint32_t q = perm[d];
-        const Binned b = bin_point(x[q], y[q], g, nb);
-        xy[d] = make_float2(b.lx, b.ly);
-        rng[d] = make_uint2(((uint32_t)b.ilo & 0xffffu) | ((uint32_t)b.ihi << 16),
-                            ((uint32_t)b.jlo & 0xffffu) | ((uint32_t)b.jhi << 16));
+    constexpr int U = 4;
+    const int tile = blockDim.x * U;
+    for (int d0 = blockIdx.x * tile + threadIdx.x; d0 < nbin; d0 += gridDim.x * tile) {
+        uint32_t q[U];
+        double xv[U], yv[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int d = d0 + u * blockDim.x;
+            q[u] = d < nbin ? perm[d] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int d = d0 + u * blockDim.x;
+            xv[u] = d < nbin ? x[q[u]] : 0.0;
+            yv[u] = d < nbin ? y[q[u]] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int d = d0 + u * blockDim.x;
+            if (d >= nbin) break;
+            const Binned b = bin_point(xv[u], yv[u], g, nb);
+            xy[d] = make_float2(b.lx, b.ly);
+            rng[d] = make_uint2(((uint32_t)b.ilo & 0xffffu) | ((uint32_t)b.ihi << 16),
+                                ((uint32_t)b.jlo & 0xffffu) | ((uint32_t)b.jhi << 16));
+        }
     }
 }
 
@@ -331,7 +364,7 @@ int bin_points(kde_ctx* c, const double* d_x, const double* d_y, int64_t n64) {
     }
     cudaMemsetAsync(c->d_stats, 0, 3 * sizeof(unsigned long long), s);
     if (n > 0) {
-        const int grid = (n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16;
+        const int grid = (n + 1023) / 1024 < 148 * 8 ? (n + 1023) / 1024 : 148 * 8;
         bin_convert_kernel<<<grid, 256, 0, s>>>(d_x, d_y, n, g, nb, pb.key[0], c->d_stats);
         c->launches += 1;
         // LSD passes over the key bits of [0, nb]
@@ -361,7 +394,7 @@ int bin_points(kde_ctx* c, const double* d_x, const double* d_y, int64_t n64) {
         pb.perm = pb.val[cur];
         const int og = (n + 1 + 255) / 256 < 148 * 16 ? (n + 1 + 255) / 256 : 148 * 16;
         offsets_kernel<<<og, 256, 0, s>>>(pb.key[cur], n, nb, c->d_offsets);
-        const int gg = (n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16;
+        const int gg = (n + 1023) / 1024 < 148 * 8 ? (n + 1023) / 1024 : 148 * 8;
         gather_kernel<<<gg, 256, 0, s>>>(d_x, d_y, pb.perm, c->d_offsets, nb, g, pb.xy, pb.rng);
         c->launches += 2;
     } else {

@@ -102,6 +102,10 @@ struct kde_ctx {
     uint32_t* d_offsets = nullptr;             // nb + 1
     unsigned long long* d_stats = nullptr;     // n_finite, n_outside, useful_pairs
     cudaEvent_t loaded_ev = nullptr;           // end of the last load (eval waits on it)
+    cudaEvent_t evald_ev = nullptr;            // end of the last eval (the next load's
+                                               // binning waits on it: eval reads the bins)
+    cudaEvent_t input_ev = nullptr;            // legacy-stream point for device inputs
+    bool evaluated = false;
     int* h_totals = nullptr;                   // pinned: plan totals + stats readback
     kde_stats stats{};
     bool loaded = false;
