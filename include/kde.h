@@ -167,7 +167,9 @@ KDE_API int kde_get_stats(const kde_ctx* c, kde_stats* s);
 /*
  * kde_get_bins: copy the binning result of the last load to HOST memory for
  * inspection (bit-exact parity tests).  Any pointer may be NULL to skip it.
- *   offsets [nbx*nby+1] int64   bucket start positions (exclusive scan of counts)
+ *   offsets [nbx*nby+1] int64   bucket start positions (exclusive scan of counts); the
+ *                               bucket key is column-major, key = bx * nby + by, with
+ *                               (bx, by) = (clamp(floor(u))/B, clamp(floor(v))/B)
  *   perm    [n_binned]  int64   original index of each sorted point
  *   lx, ly  [n_binned]  float   bucket-local coordinates u - bx*B, v - by*B (fp64->RN fp32)
  *   ranges  [4*n_binned] int32  i_lo, i_hi, j_lo, j_hi (clipped to the raster)

@@ -262,7 +262,7 @@ int64_t oracle_bin(const oracle_params *p, int32_t B, int32_t stack, const doubl
         int32_t hy = fv < 0 ? 0 : (fv > H - 1 ? H - 1 : (int32_t)fv);
         int32_t bx = hx / B, by = hy / B;
         if (by < band_lo || by > band_hi) { st->n_outside++; continue; } /* outside band reach */
-        key[q] = (int64_t)by * nbx + bx;
+        key[q] = (int64_t)bx * nby + by;               /* column-major bucket key */
         r4[4 * q + 0] = (int32_t)ilo; r4[4 * q + 1] = (int32_t)ihi;
         r4[4 * q + 2] = (int32_t)jlo; r4[4 * q + 3] = (int32_t)jhi;
         uu[q] = u; vv[q] = v;
@@ -281,7 +281,7 @@ int64_t oracle_bin(const oracle_params *p, int32_t B, int32_t stack, const doubl
     for (int64_t q = 0; q < n; q++) {
         if (key[q] < 0) continue;
         int64_t d = fill[key[q]]++;
-        int32_t bx = (int32_t)(key[q] % nbx), by = (int32_t)(key[q] / nbx);
+        int32_t bx = (int32_t)(key[q] / nby), by = (int32_t)(key[q] % nby);
         perm[d] = q;
         lx[d] = (float)(uu[q] - (double)(bx * B));  /* bucket-local, fp64 then RN to fp32 */
         ly[d] = (float)(vv[q] - (double)(by * B));

@@ -47,7 +47,7 @@ __device__ __forceinline__ Binned bin_point(double x, double y, const Geom& g, u
     const int bx = hx / g.B, by = hy / g.B;
     if (by < g.band_lo || by > g.band_hi) return b;  // outside the band's reach
     b.status = 2;
-    b.key = (uint32_t)(by * g.nbx + bx);
+    b.key = (uint32_t)(bx * g.nby + by);  // column-major: a vertical bucket stack is contiguous
     b.ilo = (int)ilo;
     b.ihi = (int)ihi;
     b.jlo = (int)jlo;

@@ -149,11 +149,12 @@ __global__ void __launch_bounds__(256) splat_kernel(const SplatArgs a) {
         const int w = s_w;
         if (w >= a.nitems) break;
         const int4 it = a.items[w];
-        const int key = it.x, sub = it.w % nsub;
+        const int gx = it.x % a.pg.ngx, gy = it.x / a.pg.ngx;  // group = one bucket (s = 1)
+        const int key = gx * g.nby + gy, sub = it.w % nsub;
         const int sx0 = (sub % nsubx) * S, sy0 = (sub / nsubx) * S;
         const int Wd = a.pg.ww;
         const int sw = min(S, Wd - sx0), sh = min(S, Wd - sy0);
-        const int bx = key % g.nbx, by = key / g.nbx;
+        const int bx = gx, by = gy;
         const int ox = bx * g.B - g.F + sx0;  // global pixel origin of the sub-window
         const int oy = by * g.B - g.F + sy0;
         const int ncx = (sw + MT - 1) / MT, ncy = (sh + MT - 1) / MT;

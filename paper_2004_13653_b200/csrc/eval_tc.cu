@@ -162,8 +162,7 @@ __global__ void __launch_bounds__(kTcThreads, 8) tc_splat_kernel(const TcArgs a)
     __shared__ __align__(8) uint64_t s_bar[3];  // operand buffers 0/1 freed; accumulator ready
     __shared__ uint32_t s_tmem;
     __shared__ int s_w;
-    __shared__ uint32_t s_pre[kMaxStack + 1];   // prefix counts of the group's buckets
-    __shared__ uint32_t s_off[kMaxStack];       // first sorted position of each bucket
+    __shared__ uint32_t s_pre[kMaxStack + 1];   // first sorted position of each stack bucket
 
     const Geom& g = a.g;
     const PathGeom& pg = a.pg;
@@ -208,27 +207,13 @@ __global__ void __launch_bounds__(kTcThreads, 8) tc_splat_kernel(const TcArgs a)
         if (t == 0) s_w = atomicAdd(&a.done[a.nslots], 1);  // pop the next item early
         const int gx = it.x % pg.ngx, gy = it.x / pg.ngx;
         const int ox = gx * pg.px - g.F, oy = gy * pg.py - g.F;  // window origin (pixels)
-        if (warp == 0) {  // bucket prefix counts and starts of this group's stack (warp scan)
-            const int by = gy * pg.s + lane;
-            uint32_t st = 0, cn = 0;
-            if (lane < pg.s && by < g.nby) {
-                const int key = by * g.nbx + gx;
-                st = a.offsets[key];
-                cn = a.offsets[key + 1] - st;
-            }
-            uint32_t inc = cn;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
-                if (lane >= o) inc += v;
-            }
-            if (lane < pg.s) {
-                s_pre[lane + 1] = inc;
-                s_off[lane] = st;
-            }
-            if (lane == 0) s_pre[0] = 0;
-        }
+        // the stack's buckets are the contiguous keys gx*nby + gy*s + k (column-major keys):
+        // s_pre[k] = first position of bucket k relative to the stack's first point
+        const int key0 = gx * g.nby + gy * pg.s;
+        const int ns = min(pg.s, g.nby - gy * pg.s);
+        if (t <= ns) s_pre[t] = a.offsets[key0 + t];
         __syncthreads();
+        const uint32_t base0 = s_pre[0];
         const int cnt = it.z - it.y;
         const int nch = (cnt + kTcChunk - 1) / kTcChunk;
         const float shx = (float)(gx * g.B - ox) - 0.5f;   // (c + 1/2) - P = c - (P - 1/2)
@@ -239,10 +224,9 @@ __global__ void __launch_bounds__(kTcThreads, 8) tc_splat_kernel(const TcArgs a)
         uint2 nr = make_uint2(0u, 0u);
         int nk = 0;
         if (q < it.z) {
-            while (kb + 1 < pg.s && (uint32_t)q >= s_pre[kb + 1]) kb++;
-            const uint32_t d = s_off[kb] + ((uint32_t)q - s_pre[kb]);
-            nl = a.xy[d];
-            nr = a.rng[d];
+            while (kb + 1 < ns && base0 + (uint32_t)q >= s_pre[kb + 1]) kb++;
+            nl = a.xy[base0 + q];
+            nr = a.rng[base0 + q];
             nk = kb;
         }
         for (int ch = 0; ch < nch; ch++) {
@@ -253,10 +237,9 @@ __global__ void __launch_bounds__(kTcThreads, 8) tc_splat_kernel(const TcArgs a)
             const bool valid = q < it.z;
             q += kTcChunk;
             if (q < it.z) {  // prefetch the next chunk's point
-                while (kb + 1 < pg.s && (uint32_t)q >= s_pre[kb + 1]) kb++;
-                const uint32_t d = s_off[kb] + ((uint32_t)q - s_pre[kb]);
-                nl = a.xy[d];
-                nr = a.rng[d];
+                while (kb + 1 < ns && base0 + (uint32_t)q >= s_pre[kb + 1]) kb++;
+                nl = a.xy[base0 + q];
+                nr = a.rng[base0 + q];
                 nk = kb;
             }
             float pxh = 0.f, pyh = 0.f;

@@ -21,16 +21,13 @@ constexpr int kPlanThreads = 256;
 constexpr int kPlanPer = 4;  // groups per thread
 constexpr int kPlanTile = kPlanThreads * kPlanPer;
 
+// Bucket keys are column-major (key = bx * nby + by), so a group -- a vertical stack of
+// pg.s buckets -- is the contiguous key range [gx*nby + gy*s, + min(s, nby - gy*s)).
 __device__ __forceinline__ uint32_t group_count(const Geom& g, const PathGeom& pg,
                                                 const uint32_t* __restrict__ off, int gx, int gy) {
-    uint32_t c = 0;
-    for (int k = 0; k < pg.s; k++) {
-        const int by = gy * pg.s + k;
-        if (by >= g.nby) break;
-        const int key = by * g.nbx + gx;
-        c += off[key + 1] - off[key];
-    }
-    return c;
+    const int k0 = gx * g.nby + gy * pg.s;
+    const int k1 = k0 + min(pg.s, g.nby - gy * pg.s);
+    return off[k1] - off[k0];
 }
 
 __device__ __forceinline__ uint64_t group_pair(const Geom& g, const PathGeom& pg,

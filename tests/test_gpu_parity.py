@@ -75,7 +75,7 @@ def test_binning_bit_exact(name, rows):
     B = got["stats"]["bucket"]
     F = int(np.floor(oracle.r_px(_grid(c)) + 0.5))
     keys = np.repeat(np.arange(len(got["offsets"]) - 1), np.diff(got["offsets"]))
-    bx, by = keys % got["stats"]["nbx"], keys // got["stats"]["nbx"]
+    bx, by = keys // got["stats"]["nby"], keys % got["stats"]["nby"]  # column-major keys
     r = got["ranges"]
     assert np.all(r[:, 0] >= bx * B - F) and np.all(r[:, 1] <= bx * B + B - 1 + F)
     assert np.all(r[:, 2] >= by * B - F) and np.all(r[:, 3] <= by * B + B - 1 + F)

@@ -53,7 +53,7 @@ def test_O8_binning_matches_definitions(B, kernel):
             continue
         hx = min(max(math.floor(u[q]), 0), g.width - 1)
         hy = min(max(math.floor(v[q]), 0), g.height - 1)
-        keys[q] = (hy // B) * r["nbx"] + hx // B
+        keys[q] = (hx // B) * r["nby"] + hy // B   # column-major bucket key
         rngs[q] = (cols[0], cols[-1], rows[0], rows[-1])
     kept = np.array(sorted(keys), dtype=np.int64)
     assert st["n_binned"] == len(kept) and st["n_outside"] == fin.sum() - len(kept)
@@ -64,7 +64,7 @@ def test_O8_binning_matches_definitions(B, kernel):
     np.testing.assert_array_equal(r["offsets"], np.r_[0, np.cumsum(counts)])
     np.testing.assert_array_equal(r["ranges"], np.array([rngs[q] for q in order]))
     ks = np.array([keys[q] for q in order])
-    bx, by = ks % r["nbx"], ks // r["nbx"]
+    bx, by = ks // r["nby"], ks % r["nby"]
     np.testing.assert_array_equal(r["lx"], (u[order] - bx * B).astype(np.float32))
     np.testing.assert_array_equal(r["ly"], (v[order] - by * B).astype(np.float32))
     rr = r["ranges"].astype(np.int64)
@@ -73,7 +73,7 @@ def test_O8_binning_matches_definitions(B, kernel):
 
 def test_O8_scan_example_spec190():
     # exclusive scan of [1,1,0,1] -> [0,1,2,2]; here as bucket counts.
-    g = oracle.Grid(0.0, 0.0, 1.0, 64, 16, 1.0, 6, 1.0)   # 4 x 1 buckets of 16
+    g = oracle.Grid(0.0, 0.0, 1.0, 64, 16, 1.0, 6, 1.0)   # 4 x 1 buckets of 16 (key = bx)
     x = np.array([20.5, 3.5, 55.5])   # buckets 1, 0, 3 -> counts [1,1,0,1]
     y = np.array([8.5, 8.5, 8.5])
     r = oracle.bin_points(g, 16, x, y)
@@ -91,7 +91,7 @@ def test_O8_band_filter_stack_rounding():
     b = oracle.bin_points(gb, 16, x, y, stack=4)
     lo, hi = ((100 // 16 - nr) // 4) * 4, ((179 // 16 + nr) // 4 + 1) * 4 - 1
     keys = np.repeat(np.arange(len(full["offsets"]) - 1), np.diff(full["offsets"]))
-    sel = (keys // full["nbx"] >= lo) & (keys // full["nbx"] <= hi)
+    sel = (keys % full["nby"] >= lo) & (keys % full["nby"] <= hi)
     np.testing.assert_array_equal(b["perm"], full["perm"][sel])
     assert lo % 4 == 0 and (hi + 1) % 4 == 0
 
@@ -110,7 +110,8 @@ def test_O8_band_filter_keeps_reach_rows_and_counts_band_pairs():
         lo, hi = rb // 16 - nr, (re - 1) // 16 + nr
         nbx = full["nbx"]
         keys = np.repeat(np.arange(len(full["offsets"]) - 1), np.diff(full["offsets"]))
-        sel = (keys // nbx >= lo) & (keys // nbx <= hi)
+        nby = full["nby"]
+        sel = (keys % nby >= lo) & (keys % nby <= hi)
         np.testing.assert_array_equal(b["perm"], full["perm"][sel])
         np.testing.assert_array_equal(b["ranges"], full["ranges"][sel])
         tot += b["stats"]["useful_pairs"]
