@@ -282,11 +282,18 @@ def run_ours(args):
                 "peak": round(peak, 2), "unit": "TFLOP/s",
                 "peak_source": "derived: 148 SMs x 128 FP32 FMA/clk x 2 x sm_max_mhz (%s)" % peak_src}
     else:
+        # tensor-pipe bound: the contraction's executed MMA flops
+        # (kde_stats.tc_mma_flops: 2 x 128 x N x 16 x 2 per 32-point chunk) per kernel time,
+        # against the fp16 dense peak; the useful-pair share of those flops next to it
         peak = peaks["bf16_tflops"]  # fp16 dense = bf16 dense rate (guide's nominal ratio 1)
+        mma = st["tc_mma_flops"]
         roof = {"bound": "tensor", "kernel": "tc_splat_kernel",
-                "achieved": 2.0 * st["useful_pairs"] / (eval_ms * 1e-3) / 1e12,
+                "achieved": mma / (eval_ms * 1e-3) / 1e12,
                 "peak": peak, "unit": "TFLOP/s",
-                "peak_source": f"{peak_src} bf16_tflops (fp16 dense rate = bf16)"}
+                "peak_source": f"{peak_src} bf16_tflops (fp16 dense rate = bf16)",
+                "mma_flops_per_launch": mma,
+                "useful_tflops": round(2.0 * st["useful_pairs"] / (eval_ms * 1e-3) / 1e12, 3),
+                "useful_share_of_mma": round(2.0 * st["useful_pairs"] / max(mma, 1), 4)}
     roof["achieved"] = round(roof["achieved"], 3)
     roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
     roof["traffic"] = _traffic(roof["kernel"])

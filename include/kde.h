@@ -113,6 +113,9 @@ typedef struct {
                               (floor(h/stack)+1)*stack - 1] with l = rb/B - nr,
                               h = (re-1)/B + nr, nr = ceil(reach_px/B)                      */
     int64_t kernel_launches; /* CUDA kernels this context has launched so far (cumulative)  */
+    int64_t tc_mma_flops;  /* tensor-core flops one KDE_PATH_TENSOR eval of the last load
+                              executes (2 per MMA multiply-add; 0 until that path has been
+                              evaluated for the load): the tensor-pipe roofline numerator   */
 } kde_stats;
 
 /*
@@ -133,10 +136,10 @@ KDE_API int kde_create(const kde_params* p, kde_ctx** out);
  *             both host pointers (copied to the device through a pinned staging
  *             buffer) or both device pointers on params.device.  Not retained.
  *   n    [in] >= 0 (0 is legal: kde_eval then writes zeros).
- * Runs a1 (fp64 convert, integer support ranges, bucket keys), a2 (stable LSD
- * counting sort by bucket key, gather to bucket-local fp32 SoA) and the
- * device-side evaluation plan on the context's internal stream, and returns
- * once the plan's totals are known (one 40-byte readback).  Ordering: device
+ * Enqueues a1 (fp64 convert, integer support ranges, bucket keys) and a2 (stable
+ * LSD counting sort by bucket key, gather to bucket-local fp32 SoA) on the
+ * context's internal stream and returns without waiting for them (the integer
+ * stats come back asynchronously; kde_get_stats waits).  Ordering: device
  * inputs are read after all work already queued on the legacy default stream
  * (PyTorch's default stream); binning starts after the context's previous
  * kde_eval has finished reading the bins; a host-input upload may overlap that
@@ -153,6 +156,10 @@ KDE_API int kde_load_points(kde_ctx* c, const double* x, const double* y, int64_
  *                (all H*W when the band is 0,0), caller-owned; fully overwritten.
  *   stream [in] cudaStream_t (NULL = legacy default stream).  Stream-ordered and
  *               asynchronous: results are ready when the stream reaches this point.
+ * The first eval of a path after a load also builds that path's device-side plan
+ * on `stream`, without a host round trip (buffers are reserved at
+ * their upper bounds; only a window so large that the bound exceeds 1/8 of device
+ * memory costs one 4-byte readback).  Evals of one context run in call order.
  * Deterministic: the same inputs give bitwise-identical output, and a banded
  * context gives exactly the rows of the unbanded raster.
  * Errors: KDE_EINVAL (NULL ctx/out, unknown path), KDE_ESTATE (no kde_load_points
@@ -161,7 +168,9 @@ KDE_API int kde_load_points(kde_ctx* c, const double* x, const double* y, int64_
  */
 KDE_API int kde_eval(kde_ctx* c, int32_t path, float* out, void* stream);
 
-/* kde_get_stats: counters of the last load (all zero before one). EINVAL on NULL. */
+/* kde_get_stats: counters of the last load (all zero before one); waits for the
+ * load's asynchronous stats readback (and reads tc_mma_flops from the device).
+ * Errors: KDE_EINVAL on NULL, KDE_ECUDA. */
 KDE_API int kde_get_stats(const kde_ctx* c, kde_stats* s);
 
 /*
@@ -183,7 +192,7 @@ KDE_API int kde_get_bins(const kde_ctx* c, int64_t* offsets, int64_t* perm, floa
  * benchmark's roofline: disabled by default; when enabled every load/eval records
  * events around its phases.  kde_get_timing synchronises on the last eval.
  *   bin_ms      a1 + a2 (convert, counting sort, gather) of the last load
- *   plan_ms     device-side plan of the last load
+ *   plan_ms     device-side plan built by the last eval (~0 when it was cached)
  *   main_ms     the evaluation kernel of the last eval (splat pass / tensor-core pass)
  *   combine_ms  the combine pass (a5) of the last eval
  * Errors: KDE_EINVAL (NULL), KDE_ESTATE (timing disabled or nothing recorded).

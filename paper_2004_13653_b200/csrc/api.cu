@@ -52,8 +52,8 @@ static int dalloc(void** p, size_t bytes, const char* what) {
 }
 
 // Direct-path geometry, fixed at create: groups are single buckets; the window B + 2F is
-// cut into equal square sub-windows of <= kSub, and the register micro-tile edge MT is the
-// one whose thread grid best fills whole warps.
+// cut into nsub x nsub equal sub-windows of <= 48 pixels, each computed by a lane grid of
+// 4 x 8 register tiles of 2TY x TY pixels (S = 8 TY >= the sub-window edge, TY in 2..6).
 static void plan_geometry_direct(EvalPlan& pl, const Geom& g) {
     PathGeom& pg = pl.pg;
     const int Wd = g.B + 2 * g.F;
@@ -62,24 +62,11 @@ static void plan_geometry_direct(EvalPlan& pl, const Geom& g) {
     pg.ngy = g.nby;
     pg.px = pg.py = g.B;
     pg.ww = pg.wh = Wd;
-    pg.nsubx = pg.nsuby = (Wd + kSub - 1) / kSub;
+    pg.nsubx = pg.nsuby = (Wd + kSubMax - 1) / kSubMax;
     pg.sx = pg.sy = (Wd + pg.nsubx - 1) / pg.nsubx;  // the last sub-window may be smaller
-    double best = -1.0;
-    for (int mt = 3; mt <= 6; mt++) {
-        const int nm = (pg.sx + mt - 1) / mt;
-        if (nm * nm > 256) continue;
-        const int thr = ((nm * nm + 31) / 32) * 32;
-        const double cover = (double)pg.sx / (nm * mt);
-        const double util = cover * cover * (double)(nm * nm) / thr + 1e-3 * mt;
-        if (util > best) {
-            best = util;
-            pl.mt = mt;
-            pl.threads = thr;
-        }
-    }
-    const int nm = (pg.sx + pl.mt - 1) / pl.mt;
-    pg.slot_w = pg.slot_h = ((nm * pl.mt + 3) / 4) * 4;  // float4-aligned slots
-    pl.ld = nm * (pl.mt <= 4 ? 4 : 8) + 4;
+    pl.mt = std::max(2, (pg.sx + 7) / 8);            // TY
+    pg.slot_w = pg.slot_h = 8 * pl.mt;               // S x S slot (float4-aligned rows)
+    pg.part_pts = kPartPtsDirect;                    // remainders: one warp per 128 points
     pl.enabled = true;
 }
 
@@ -112,7 +99,7 @@ static int alloc_plan(EvalPlan& pl) {
     cudaError_t e = cudaMalloc(&pl.d_local, sizeof(uint64_t) * nblk * 1024);
     if (e == cudaSuccess) e = cudaMalloc(&pl.d_bsum, sizeof(uint64_t) * (nblk + 1));
     if (e == cudaSuccess) e = cudaMalloc(&pl.d_group, sizeof(int2) * (ng > 0 ? ng : 1));
-    if (e == cudaSuccess) e = cudaMalloc(&pl.d_totals, sizeof(int) * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&pl.d_totals, sizeof(int) * kTotInts);
     if (e == cudaSuccess) e = cudaMalloc(&pl.d_hot, sizeof(int) * (ng > 0 ? ng : 1));
     if (e != cudaSuccess) {
         cudaGetLastError();
@@ -122,35 +109,52 @@ static int alloc_plan(EvalPlan& pl) {
     return KDE_OK;
 }
 
-// before planning: the item list at its upper bound (full segments + one partial per
-// group), so the plan can write it without a host round trip
-static int reserve_items(EvalPlan& pl, int64_t n) {
-    if (!pl.enabled) return KDE_OK;
-    const int64_t bound = (n / kSegPts + std::min<int64_t>(n, pl.pg.ngroups())) * pl.pg.nsub() + 1;
-    if (bound > pl.items_cap) {
-        if (dalloc((void**)&pl.d_items, sizeof(int4) * bound, "plan items")) return KDE_ENOMEM;
-        pl.items_cap = bound;
+// Build path pl's plan for the current load on stream s.  The item list
+// and the splat buffer are reserved at their upper bounds, so the plan needs no host round
+// trip -- unless the splat bound exceeds the context's budget (very large windows): then
+// the exact slot count is read back once and only that much is allocated.
+static int plan_path(kde_ctx* c, EvalPlan& pl, cudaStream_t s) {
+    const int64_t bound = slot_bound(pl.pg, c->stats.n_in);
+    if (bound + 1 > pl.items_cap) {
+        if (dalloc((void**)&pl.d_items, sizeof(int4) * (bound + 1), "plan items")) return KDE_ENOMEM;
+        pl.items_cap = bound + 1;
     }
+    const size_t slot_bytes = sizeof(float) * (size_t)pl.pg.slot_floats();
+    const bool exact = (size_t)bound * slot_bytes > c->splat_budget;
+    if (!exact && bound > pl.slots_cap) {
+        if (dalloc((void**)&pl.d_splat, slot_bytes * (size_t)(bound > 0 ? bound : 1), "splat blocks"))
+            return KDE_ENOMEM;
+        pl.slots_cap = bound;
+    }
+    int rc = plan_device(c, pl, s);
+    if (rc) return rc;
+    if (exact) {
+        int nslots = 0;
+        cudaError_t e = cudaMemcpyAsync(c->h_totals, pl.d_totals + kTotSlots, sizeof(int),
+                                        cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return cuda_fail(e, "kde_eval: plan readback");
+        nslots = c->h_totals[0];
+        if (nslots > pl.slots_cap) {
+            if (dalloc((void**)&pl.d_splat, slot_bytes * (size_t)nslots, "splat blocks")) return KDE_ENOMEM;
+            pl.slots_cap = nslots;
+        }
+    }
+    pl.planned_gen = c->load_gen;
     return KDE_OK;
 }
 
-// after the totals are known: splat capacity
-static int finish_plan(EvalPlan& pl, const int* tot) {
-    if (!pl.enabled) return KDE_OK;
-    const int nsub = pl.pg.nsub();
-    pl.tf = tot[0];
-    pl.tp = tot[1];
-    pl.nslots = tot[2];
-    pl.nitems = (pl.tf + pl.tp) * nsub;
-    pl.nhot = tot[4];
-    if (pl.nslots > pl.slots_cap) {
-        if (dalloc((void**)&pl.d_splat, sizeof(float) * (size_t)pl.nslots * pl.pg.slot_floats(),
-                   "splat blocks"))
-            return KDE_ENOMEM;
-        if (dalloc((void**)&pl.d_done, sizeof(int) * ((size_t)pl.nslots + 1), "splat counters"))
-            return KDE_ENOMEM;
-        pl.slots_cap = pl.nslots;
-    }
+// fold the load's asynchronous stats readback into c->stats (waits for it)
+static int sync_stats(kde_ctx* c) {
+    if (!c->stats_pending) return KDE_OK;
+    const cudaError_t e = cudaEventSynchronize(c->stats_ev);
+    if (e != cudaSuccess) return cuda_fail(e, "stats readback");
+    const unsigned long long* st = reinterpret_cast<const unsigned long long*>(c->h_totals + 16);
+    c->stats.n_finite = (int64_t)st[0];
+    c->stats.n_outside = (int64_t)st[1];
+    c->stats.useful_pairs = (int64_t)st[2];
+    c->stats.n_binned = (int64_t)(uint32_t)c->h_totals[24];
+    c->stats_pending = false;
     return KDE_OK;
 }
 
@@ -162,7 +166,6 @@ static void free_plan(EvalPlan& pl) {
     cudaFree(pl.d_hot);
     cudaFree(pl.d_items);
     cudaFree(pl.d_splat);
-    cudaFree(pl.d_done);
     pl = EvalPlan();
 }
 
@@ -289,6 +292,12 @@ int kde_create(const kde_params* p, kde_ctx** out) {
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->loaded_ev, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->evald_ev, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->input_ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->stats_ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) {
+        size_t fr = 0, tot = 0;
+        e = cudaMemGetInfo(&fr, &tot);
+        c->splat_budget = std::min<size_t>(tot / 8, (size_t)16 << 30);
+    }
     if (e == cudaSuccess) e = cudaMallocHost(&c->h_totals, 128);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_offsets, sizeof(uint32_t) * (nb + 1));
     if (e == cudaSuccess) e = cudaMalloc(&c->d_stats, sizeof(unsigned long long) * 4);
@@ -368,33 +377,19 @@ int kde_load_points(kde_ctx* c, const double* x, const double* y, int64_t n) {
     int rc = bin_points(c, dx, dy, n);
     if (rc) return rc;
     tmark(c, 1, c->stream);
-    for (int p = 0; p < 2; p++)
-        if (c->plan[p].enabled) {
-            if (reserve_items(c->plan[p], n)) return KDE_ENOMEM;
-            rc = plan_device(c, c->plan[p]);
-            if (rc) return rc;
-        }
-    tmark(c, 2, c->stream);
     c->tev_load = c->timing;
-    // one small readback: plan totals of both paths + the integer stats
-    for (int p = 0; p < 2; p++)
-        if (c->plan[p].enabled)
-            cudaMemcpyAsync(c->h_totals + 8 * p, c->plan[p].d_totals, 5 * sizeof(int),
-                            cudaMemcpyDeviceToHost, c->stream);
-    cudaMemcpyAsync(c->h_totals + 16, c->d_stats, 3 * sizeof(unsigned long long),
-                    cudaMemcpyDeviceToHost, c->stream);
-    cudaError_t e = cudaStreamSynchronize(c->stream);
-    if (e != cudaSuccess) return cuda_fail(e, "kde_load_points");
-    const unsigned long long* st = reinterpret_cast<const unsigned long long*>(c->h_totals + 16);
+    // the integer stats come back asynchronously (kde_get_stats waits for them); the
+    // per-path plans are built lazily by the first kde_eval of each path
     c->stats.n_in = n;
-    c->stats.n_finite = (int64_t)st[0];
-    c->stats.n_outside = (int64_t)st[1];
-    c->stats.useful_pairs = (int64_t)st[2];
-    c->stats.n_binned = (int64_t)(c->plan[KDE_PATH_DIRECT].enabled ? c->h_totals[3] : c->h_totals[8 + 3]);
-    for (int p = 0; p < 2; p++) {
-        rc = finish_plan(c->plan[p], c->h_totals + 8 * p);
-        if (rc) return rc;
-    }
+    c->stats.n_finite = c->stats.n_binned = c->stats.n_outside = c->stats.useful_pairs = 0;
+    cudaMemcpyAsync(c->h_totals + 16, c->d_stats, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                    c->stream);
+    cudaMemcpyAsync(c->h_totals + 24, c->d_offsets + (size_t)c->g.nbx * c->g.nby, sizeof(uint32_t),
+                    cudaMemcpyDeviceToHost, c->stream);
+    cudaError_t e = cudaEventRecord(c->stats_ev, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "kde_load_points: event");
+    c->stats_pending = true;
+    c->load_gen++;
     e = cudaEventRecord(c->loaded_ev, c->stream);
     if (e != cudaSuccess) return cuda_fail(e, "kde_load_points: event");
     c->loaded = true;
@@ -424,8 +419,15 @@ int kde_eval(kde_ctx* c, int32_t path, float* out, void* stream) {
     cudaError_t e = cudaGetLastError();  // surface earlier asynchronous faults
     if (e != cudaSuccess) return cuda_fail(e, "kde_eval: earlier asynchronous error");
     cudaStream_t s = (cudaStream_t)stream;
-    e = cudaStreamWaitEvent(s, c->loaded_ev, 0);  // the plan of the last load
+    e = cudaStreamWaitEvent(s, c->loaded_ev, 0);  // the bins of the last load
+    if (e == cudaSuccess && c->evaluated) e = cudaStreamWaitEvent(s, c->evald_ev, 0);  // evals in order
     if (e != cudaSuccess) return cuda_fail(e, "kde_eval: wait for load");
+    EvalPlan& pl = c->plan[path];
+    tmark(c, 2, s);
+    if (pl.planned_gen != c->load_gen) {
+        const int prc = plan_path(c, pl, s);
+        if (prc) return prc;
+    }
     const int rc = path == KDE_PATH_DIRECT ? launch_direct(c, out, s) : launch_tc(c, out, s);
     if (rc == KDE_OK) {
         cudaEventRecord(c->evald_ev, s);
@@ -459,10 +461,10 @@ int kde_get_timing(kde_ctx* c, kde_timing* t) {
     }
     DeviceGuard dg(c->p.device);
     cudaError_t e = cudaEventSynchronize(c->tev[5]);
-    if (e == cudaSuccess) e = cudaEventSynchronize(c->tev[2]);
+    if (e == cudaSuccess) e = cudaEventSynchronize(c->tev[1]);
     if (e != cudaSuccess) return cuda_fail(e, "kde_get_timing");
     cudaEventElapsedTime(&t->bin_ms, c->tev[0], c->tev[1]);
-    cudaEventElapsedTime(&t->plan_ms, c->tev[1], c->tev[2]);
+    cudaEventElapsedTime(&t->plan_ms, c->tev[2], c->tev[3]);
     cudaEventElapsedTime(&t->main_ms, c->tev[3], c->tev[4]);
     cudaEventElapsedTime(&t->combine_ms, c->tev[4], c->tev[5]);
     return KDE_OK;
@@ -473,8 +475,21 @@ int kde_get_stats(const kde_ctx* c, kde_stats* s) {
         set_error("kde_get_stats: NULL argument");
         return KDE_EINVAL;
     }
+    kde_ctx* m = const_cast<kde_ctx*>(c);
+    DeviceGuard dg(c->p.device);
+    int rc = sync_stats(m);
+    if (rc) return rc;
     *s = c->stats;
     s->kernel_launches = c->launches;
+    s->tc_mma_flops = 0;
+    const EvalPlan& tp = c->plan[KDE_PATH_TENSOR];
+    if (c->loaded && tp.enabled && tp.planned_gen == c->load_gen) {  // executed MMA flops / eval
+        int chunks = 0;
+        const cudaError_t e = cudaMemcpy(&chunks, tp.d_totals + kTotChunks, sizeof(int), cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return cuda_fail(e, "kde_get_stats");
+        // per 32-point chunk: two M=128 x N x K=16 MMAs, 2 flops per MAC
+        s->tc_mma_flops = (int64_t)chunks * 2 * 2 * kTcM * tp.pg.slot_w * 16;
+    }
     return KDE_OK;
 }
 
@@ -489,6 +504,7 @@ int kde_get_bins(const kde_ctx* c, int64_t* offsets, int64_t* perm, float* lx, f
         return KDE_ESTATE;
     }
     DeviceGuard dg(c->p.device);
+    if (int rc = sync_stats(const_cast<kde_ctx*>(c))) return rc;
     const size_t nb = (size_t)c->g.nbx * c->g.nby;
     const size_t m = (size_t)c->stats.n_binned;
     if (cudaEventSynchronize(c->loaded_ev) != cudaSuccess) return cuda_fail(cudaGetLastError(), "kde_get_bins");
@@ -556,6 +572,7 @@ void kde_free(kde_ctx* c) {
     if (c->loaded_ev) cudaEventDestroy(c->loaded_ev);
     if (c->evald_ev) cudaEventDestroy(c->evald_ev);
     if (c->input_ev) cudaEventDestroy(c->input_ev);
+    if (c->stats_ev) cudaEventDestroy(c->stats_ev);
     for (int k = 0; k < 6; k++)
         if (c->tev[k]) cudaEventDestroy(c->tev[k]);
     if (c->h_totals) cudaFreeHost(c->h_totals);

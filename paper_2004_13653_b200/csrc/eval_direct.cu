@@ -9,19 +9,24 @@
 // anchorages: >90% of points share an 8x8-pixel home bucket with >=128 others), so the
 // register tiles are aligned to the POINT GROUPS instead of the output grid:
 //
-//   splat pass   one CTA per (bucket g, segment of <= 1024 of its points, 64x64 sub-window
-//                of g's window [bx*B - F, bx*B + B - 1 + F]^2, F = floor(R + 1/2)).  Per
-//                chunk of 32 points the CTA evaluates the 1-D factors khat(s) for the
-//                window's columns and khat(t) for its rows once into shared memory
-//                (masked by the fp64-decided integer ranges; double-buffered, one barrier
-//                per chunk), and each thread accumulates a 4x4 register micro-tile with one
-//                FFMA per (pixel, point) pair: acc += ky[r] * kx[c].  Blocked fp32
-//                accumulation (per-chunk partials into running totals, R10).
-//                The block is written to its splat slot.
+//   splat pass   persistent CTAs of 8 warps pop work items (bucket g, segment of <= 512
+//                of its points, sub-window S x S of g's window [bx*B - F, bx*B+B-1+F]^2,
+//                F = floor(R + 1/2)).  The warps split the segment into 16-point chunks
+//                (warp w takes chunks w, w+8, ...) and work without CTA barriers: per
+//                chunk the warp evaluates the 1-D factors of its 16 points into its own
+//                shared-memory buffer (lanes 0-15: the S column factors khat(s) of point
+//                lane, lanes 16-31: the S row factors khat(t); masked by the fp64-decided
+//                integer ranges), __syncwarp, and every lane accumulates a TY x 2TY
+//                register tile (lanes = 4 column groups x 8 row groups, S = 8 TY) with one
+//                FFMA per (pixel, point) pair: acc += ky[r] * kx[c] -- 5 vector LDS per
+//                50 FFMA at S = 40.  At the end of the item the warps' tiles are summed in
+//                a fixed order (warp 0..7) through shared memory into the segment's slot.
 //   combine pass one CTA per 32x32 output tile sums, for every pixel, the splat blocks of
 //                the groups whose window covers it, in a fixed order (group row-major, then
 //                segment), and multiplies by C/(n h_px^2) (step a5).  Deterministic; a band
 //                computes exactly the same splats, so sharded == unsharded bitwise.
+#include <algorithm>
+
 #include "internal.cuh"
 #include "kernels.cuh"
 
@@ -34,200 +39,235 @@ struct SplatArgs {
     const uint2* __restrict__ rng;
     const int4* __restrict__ items;   // (bucket, k0, k1, slot)
     const int2* __restrict__ group;   // per bucket: (slot of segment 0, #segments)
-    int* __restrict__ done;           // per slot arrival counters; done[nslots] = work queue
+    int* __restrict__ totals;         // plan totals (kTot*): item count, work-queue head
     float* __restrict__ splat;
     PathGeom pg;
-    int nitems, nslots;
     KConst k;
     float c2;     // radial: c_eff^2
     float q2;     // Gaussian recurrence step 2^(2 kq)
     bool recur;   // recurrence safe: 2^(kq (R + 8)^2) stays a normal float
-    int ld;       // factor row stride (floats)
 };
 
-constexpr int kChunk = 32;         // points per factor chunk (one per lane)
+constexpr int kWarps = 8;     // warps per splat CTA
+constexpr int kWChunk = 16;   // points per warp chunk
 
 __device__ __forceinline__ int floor_div(int a, int b) {
     return a >= 0 ? a / b : -((-a + b - 1) / b);
 }
 
-// factor-row stride per micro-tile column group (floats): keeps vector loads aligned
-template <int MT>
-constexpr int mt_stride() { return MT <= 4 ? 4 : 8; }
+// Shared-memory layout of one warp's factor buffer for lane tile TY x TX (TX = 2 TY):
+// per point, 4 column groups of TX floats (stride TXP) then 8 row groups of TY floats
+// (stride TYP, skewed by 4 floats after group 3 when TYP = 8) -- every vector load of the
+// consume loop is 16-byte aligned and the 4 (8) groups a warp reads hit distinct banks.
+template <int TY>
+struct WLayout {
+    static constexpr int TX = 2 * TY, S = 8 * TY;
+    static constexpr int TXP = (TX + 3) / 4 * 4, TYP = (TY + 3) / 4 * 4;
+    static constexpr int COLS = 4 * TXP;
+    static constexpr int SKEW = TYP == 8 ? 4 : 0;
+    static constexpr int LDP = COLS + 8 * TYP + SKEW;  // floats per point (multiple of 4)
+    static constexpr int FACT_FLOATS = kWarps * kWChunk * LDP;
+    static constexpr int RED_FLOATS = kWarps * S * S;
+    static constexpr int SMEM_FLOATS = FACT_FLOATS > RED_FLOATS ? FACT_FLOATS : RED_FLOATS;
+    __device__ static int rowoff(int my) { return COLS + my * TYP + (my >= 4 ? SKEW : 0); }
+};
 
-template <int MT>
-__device__ __forceinline__ void lds_mt(const float* p, float (&v)[MT]) {
-    if constexpr (MT == 3) {
-        const float2 a = *reinterpret_cast<const float2*>(p);
-        v[0] = a.x; v[1] = a.y; v[2] = p[2];
-    } else if constexpr (MT == 4) {
-        const float4 a = *reinterpret_cast<const float4*>(p);
-        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-    } else if constexpr (MT == 5) {
-        const float4 a = *reinterpret_cast<const float4*>(p);
-        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = p[4];
-    } else {
-        const float4 a = *reinterpret_cast<const float4*>(p);
-        const float2 b = *reinterpret_cast<const float2*>(p + 4);
-        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y;
+// N consecutive floats from a 16-byte aligned shared address, widest loads first
+template <int N>
+__device__ __forceinline__ void lds_n(const float* p, float* v) {
+#pragma unroll
+    for (int k = 0; k + 4 <= N; k += 4) {
+        const float4 a = *reinterpret_cast<const float4*>(p + k);
+        v[k] = a.x; v[k + 1] = a.y; v[k + 2] = a.z; v[k + 3] = a.w;
     }
+    constexpr int k2 = N / 4 * 4;
+    if constexpr (N - k2 >= 2) {
+        const float2 a = *reinterpret_cast<const float2*>(p + k2);
+        v[k2] = a.x; v[k2 + 1] = a.y;
+    }
+    if constexpr ((N - k2) % 2 == 1) v[N - 1] = p[N - 1];
 }
 
-template <int MT>
-__device__ __forceinline__ void sts_mt(float* p, const float (&v)[MT]) {
-    if constexpr (MT == 3) {
-        *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
-        p[2] = v[2];
-    } else if constexpr (MT == 4) {
-        *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
-    } else if constexpr (MT == 5) {
-        *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
-        p[4] = v[4];
-    } else {
-        *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
-        *reinterpret_cast<float2*>(p + 4) = make_float2(v[4], v[5]);
-    }
-}
-
-// Factors of one point for units u = warp, warp + nwarps, ... of MT consecutive columns:
-// row[u*ST + e] = [c in range] * khat(c + 1/2 - P) for c = u*MT + e; ph = P - 1/2 in
-// sub-window coordinates, [lo, lo + span] the point's integer range (lo huge: no point).
-// The range test is a per-unit bitmask; the Gaussian uses the exact-ratio recurrence
-// g(d+1) = g(d) * r(d), r(d+1) = r(d) * 2^(2 kq) (2 FMUL per factor, 2 SFU ops per unit).
-template <int KERN, bool RADIAL, int MT>
-__device__ __forceinline__ void factor_units(float* row, int nunits, int warp, int nwarps, float ph,
-                                             int lo, int span, const SplatArgs& a) {
-    constexpr int ST = mt_stride<MT>();
-    for (int u = warp; u < nunits; u += nwarps) {
-        const int c0 = u * MT;
-        const int l0 = max(lo - c0, 0), h0 = min(lo + span - c0, MT - 1);
+// The 8 units of TY factors of one point along one axis: unit u covers sub-window
+// coordinates c = u*TY + e; f = [c in range] * khat(c + 1/2 - P), ph = P - 1/2 in
+// sub-window coordinates, [lo, lo + span] the point's integer range along the axis.
+// The Gaussian uses the exact-ratio recurrence g(d+1) = g(d) r(d), r(d+1) = r(d) 2^(2kq)
+// (2 FMUL per factor, reseeded per unit); radial forms store s^2 (or +inf when masked).
+template <int KERN, bool RADIAL, int TY>
+__device__ __forceinline__ void factor_axis(float* dst_pt, bool yaxis, float ph, int lo, int span,
+                                            const SplatArgs& a) {
+    using L = WLayout<TY>;
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+        const int c0 = u * TY;
+        const int l0 = max(lo - c0, 0), h0 = min(lo + span - c0, TY - 1);
         const uint32_t m = (l0 <= h0) ? ((2u << h0) - (1u << l0)) : 0u;
         const float d0 = (float)c0 - ph;
-        float f[MT];
+        float f[TY];
         if (!RADIAL && KERN == 6 && a.recur) {
             float gv = ex2_ftz(d0 * d0 * a.k.kq);
             float r = ex2_ftz(fmaf(2.0f, d0, 1.0f) * a.k.kq);
-            const float q = a.q2;
 #pragma unroll
-            for (int e = 0; e < MT; e++) {
+            for (int e = 0; e < TY; e++) {
                 f[e] = (m & (1u << e)) ? gv : 0.f;
                 gv *= r;
-                r *= q;
+                r *= a.q2;
             }
         } else {
 #pragma unroll
-            for (int e = 0; e < MT; e++) {
+            for (int e = 0; e < TY; e++) {
                 const float d = d0 + (float)e;
                 if constexpr (RADIAL) f[e] = (m & (1u << e)) ? d * d * a.k.inv_h2 : __int_as_float(0x7f800000);
                 else f[e] = (m & (1u << e)) ? khat<KERN>(d, a.k) : 0.f;
             }
         }
-        sts_mt<MT>(row + u * ST, f);
+        float* dst = dst_pt + (yaxis ? L::rowoff(u) : (u >> 1) * L::TXP + (u & 1) * TY);
+#pragma unroll
+        for (int e = 0; e < TY; e++) dst[e] = f[e];
     }
 }
 
-// Splat pass (see the header comment).  MT x MT register micro-tile per thread; the plan
-// picks MT in {3,4,5,6} so that ceil(S/MT)^2 threads tile the sub-window S x S with full
-// warps.  Dynamic shared memory: one factor buffer of kChunk x ld floats for columns and
-// one for rows, ld = ceil(S/MT) * mt_stride + 4 (two barriers per chunk).
-template <int KERN, bool RADIAL, int MT>
-__global__ void __launch_bounds__(256) splat_kernel(const SplatArgs a) {
-    constexpr int ST = mt_stride<MT>();
+// Item geometry shared by the two phases of the splat kernel.
+struct ItemGeo {
+    uint32_t base;  // first sorted position of the item's points
+    int cnt;        // points
+    int oo;         // sub-window origin along this lane's generation axis (pixels)
+    float sh;       // bucket-local -> sub-window coordinate shift minus 1/2, same axis
+};
+
+__device__ __forceinline__ ItemGeo item_geo(const SplatArgs& a, const int4& it, bool yaxis) {
+    const Geom& g = a.g;
+    const int nsub = a.pg.nsub(), SX = a.pg.sx;
+    const int gx = it.x % a.pg.ngx, gy = it.x / a.pg.ngx;  // group = one bucket (s = 1)
+    const int sub = it.w % nsub;
+    const int ox = gx * g.B - g.F + (sub % a.pg.nsubx) * SX;  // global pixel origin of the
+    const int oy = gy * g.B - g.F + (sub / a.pg.nsubx) * SX;  // sub-window
+    ItemGeo r;
+    r.base = a.offsets[gx * g.nby + gy] + (uint32_t)it.y;
+    r.cnt = it.z - it.y;
+    r.oo = yaxis ? oy : ox;
+    // exact small-integer shift, minus 1/2
+    r.sh = yaxis ? (float)(gy * g.B - oy) - 0.5f : (float)(gx * g.B - ox) - 0.5f;
+    return r;
+}
+
+// Accumulate chunks ch0, ch0 + step, ... of an item into the lane's register tile, using
+// this warp's factor buffer wbuf (warp-synchronous; no CTA barrier).
+template <int KERN, bool RADIAL, int TY>
+__device__ __forceinline__ void run_chunks(float (&acc)[TY][2 * TY], const SplatArgs& a, const ItemGeo& ig,
+                                           float* wbuf, int ch0, int step, int lane) {
+    using L = WLayout<TY>;
+    constexpr int TX = L::TX;
+    const int mx = lane & 3, my = lane >> 2;  // lane tile: columns mx*TX.., rows my*TY..
+    const int gp = lane & 15;                 // generation: point of this lane
+    const bool yaxis = lane >= 16;            //             and its axis
+    const int nch = (ig.cnt + kWChunk - 1) / kWChunk;
+    const float* fxp = wbuf + mx * L::TXP;
+    const float* fyp = wbuf + L::rowoff(my);
+    for (int ch = ch0; ch < nch; ch += step) {
+        const int q = ch * kWChunk + gp;
+        if (q < ig.cnt) {  // 1-D factors of point q along this lane's axis
+            const float2 l = a.xy[ig.base + q];
+            const uint2 rr = a.rng[ig.base + q];
+            const uint32_t pr = yaxis ? rr.y : rr.x;
+            const int lo = (int)(pr & 0xffffu) - ig.oo, hi = (int)(pr >> 16) - ig.oo;
+            factor_axis<KERN, RADIAL, TY>(wbuf + gp * L::LDP, yaxis, (yaxis ? l.y : l.x) + ig.sh, lo, hi - lo, a);
+        }
+        __syncwarp();
+        const int np = min(kWChunk, ig.cnt - ch * kWChunk);
+#pragma unroll 2
+        for (int p = 0; p < np; p++) {
+            float vx[TX], vy[TY];
+            lds_n<TX>(fxp + p * L::LDP, vx);
+            lds_n<TY>(fyp + p * L::LDP, vy);
+#pragma unroll
+            for (int r = 0; r < TY; r++)
+#pragma unroll
+                for (int c = 0; c < TX; c++) {
+                    if constexpr (RADIAL) {
+                        const float r2 = vx[c] + vy[r];
+                        acc[r][c] += (r2 <= a.c2) ? khat_r<KERN>(r2) : 0.f;
+                    } else {
+                        acc[r][c] = fmaf(vy[r], vx[c], acc[r][c]);
+                    }
+                }
+        }
+        __syncwarp();
+    }
+}
+
+// Splat pass.  Phase 1: the CTA's 8 warps share each full segment (warp w takes chunks
+// w, w+8, ...; tiles summed in warp order through shared memory).  Phase 2: every warp
+// alone pops remainder pieces (<= 128 points) and writes its tile straight to the slot.
+template <int KERN, bool RADIAL, int TY>
+__global__ void __launch_bounds__(kWarps * 32, 2) splat_kernel(const SplatArgs a) {
+    using L = WLayout<TY>;
+    constexpr int TX = L::TX, S = L::S;
     extern __shared__ __align__(16) float smem[];
     __shared__ int s_w;
-    const Geom& g = a.g;
-    const int ld = a.ld;
-    float* s_fx = smem;                      // [kChunk][ld]
-    float* s_fy = smem + kChunk * ld;        // [kChunk][ld]
-    const int t = threadIdx.x, warp = t >> 5, lane = t & 31, nwarps = blockDim.x >> 5;
-    const int nsubx = a.pg.nsubx, nsub = a.pg.nsub(), S = a.pg.sx, slot_ld = a.pg.slot_w;
-    const int slot_floats = slot_ld * slot_ld;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const int mx = lane & 3, my = lane >> 2;
+    const bool yaxis = lane >= 16;
+    const int slot_floats = S * S;
+    const int nsub = a.pg.nsub();
+    const int ncoop = a.totals[kTotFull] * nsub;  // full-segment items come first
+    const int nitems = a.totals[kTotSlots];
+    float* wbuf = smem + warp * (kWChunk * L::LDP);  // this warp's factor buffer
 
-    for (;;) {  // persistent: items from the queue, full segments first (equal work)
-        if (t == 0) s_w = atomicAdd(&a.done[a.nslots], 1);
+    for (;;) {  // phase 1 (persistent, CTA-cooperative)
+        if (t == 0) s_w = atomicAdd(&a.totals[kTotQueue], 1);
         __syncthreads();
         const int w = s_w;
-        if (w >= a.nitems) break;
+        if (w >= ncoop) break;
         const int4 it = a.items[w];
-        const int gx = it.x % a.pg.ngx, gy = it.x / a.pg.ngx;  // group = one bucket (s = 1)
-        const int key = gx * g.nby + gy, sub = it.w % nsub;
-        const int sx0 = (sub % nsubx) * S, sy0 = (sub / nsubx) * S;
-        const int Wd = a.pg.ww;
-        const int sw = min(S, Wd - sx0), sh = min(S, Wd - sy0);
-        const int bx = gx, by = gy;
-        const int ox = bx * g.B - g.F + sx0;  // global pixel origin of the sub-window
-        const int oy = by * g.B - g.F + sy0;
-        const int ncx = (sw + MT - 1) / MT, ncy = (sh + MT - 1) / MT;
-        const bool active = t < ncx * ncy;
-        const int mx = active ? t % ncx : 0, my = active ? t / ncx : 0;
-        // bucket-local -> sub-window coordinates (exact small-integer shift), minus 1/2
-        const float shx = (float)(bx * g.B - ox) - 0.5f, shy = (float)(by * g.B - oy) - 0.5f;
-        const uint32_t base = a.offsets[key] + (uint32_t)it.y;
-        const int cnt = it.z - it.y;
-
-        float acc[MT][MT];
+        const ItemGeo ig = item_geo(a, it, yaxis);
+        float acc[TY][TX];
 #pragma unroll
-        for (int r = 0; r < MT; r++)
+        for (int r = 0; r < TY; r++)
 #pragma unroll
-            for (int c = 0; c < MT; c++) acc[r][c] = 0.f;
-
-        // lane p of every warp holds point p of the current chunk (coalesced, prefetched)
-        float2 nxy = make_float2(0.f, 0.f);
-        uint2 nrg = make_uint2(1u, 0u);
-        if (lane < cnt) {
-            nxy = a.xy[base + lane];
-            nrg = a.rng[base + lane];
+            for (int c = 0; c < TX; c++) acc[r][c] = 0.f;
+        run_chunks<KERN, RADIAL, TY>(acc, a, ig, wbuf, warp, kWarps, lane);
+        __syncthreads();  // every warp is done with its factor buffer
+        {
+            float* red = smem + warp * (S * S) + (my * TY) * S + mx * TX;
+#pragma unroll
+            for (int r = 0; r < TY; r++)
+#pragma unroll
+                for (int c = 0; c < TX; c += 2)
+                    *reinterpret_cast<float2*>(red + r * S + c) = make_float2(acc[r][c], acc[r][c + 1]);
         }
-        const int nch = (cnt + kChunk - 1) / kChunk;
-        for (int ch = 0; ch < nch; ch++) {
-            const int np = min(kChunk, cnt - ch * kChunk);
-            const float pxh = nxy.x + shx, pyh = nxy.y + shy;
-            const int ilo = (int)(nrg.x & 0xffffu) - ox, ihi = (int)(nrg.x >> 16) - ox;
-            const int jlo = (int)(nrg.y & 0xffffu) - oy, jhi = (int)(nrg.y >> 16) - oy;
-            const bool valid = lane < np;
-            {  // prefetch the next chunk's point
-                const int q = (ch + 1) * kChunk + lane;
-                if (q < cnt) {
-                    nxy = a.xy[base + q];
-                    nrg = a.rng[base + q];
-                }
+        __syncthreads();
+        float* sp = a.splat + (size_t)it.w * slot_floats;
+        for (int e = t * 4; e < slot_floats; e += kWarps * 32 * 4) {
+            float4 v = *reinterpret_cast<const float4*>(smem + e);
+#pragma unroll
+            for (int k = 1; k < kWarps; k++) {
+                const float4 u = *reinterpret_cast<const float4*>(smem + k * (S * S) + e);
+                v.x += u.x; v.y += u.y; v.z += u.z; v.w += u.w;
             }
-            __syncthreads();  // previous chunk's factors consumed (and s_w read)
-            // 1-D factors of the lane's own point, MT columns (then MT rows) per unit
-            factor_units<KERN, RADIAL, MT>(s_fx + lane * ld, ncx, warp, nwarps, pxh,
-                                           valid ? ilo : (1 << 29), ihi - ilo, a);
-            factor_units<KERN, RADIAL, MT>(s_fy + lane * ld, ncy, warp, nwarps, pyh,
-                                           valid ? jlo : (1 << 29), jhi - jlo, a);
-            __syncthreads();
-            if (active) {
-                const float* fxp = s_fx + mx * ST;
-                const float* fyp = s_fy + my * ST;
-#pragma unroll 4
-                for (int p = 0; p < np; p++) {
-                    float vx[MT], vy[MT];
-                    lds_mt<MT>(fxp + p * ld, vx);
-                    lds_mt<MT>(fyp + p * ld, vy);
-#pragma unroll
-                    for (int r = 0; r < MT; r++)
-#pragma unroll
-                        for (int c = 0; c < MT; c++) {
-                            if constexpr (RADIAL) {
-                                const float r2 = vx[c] + vy[r];
-                                acc[r][c] += (r2 <= a.c2) ? khat_r<KERN>(r2) : 0.f;
-                            } else {
-                                acc[r][c] = fmaf(vy[r], vx[c], acc[r][c]);
-                            }
-                        }
-                }
-            }
+            *reinterpret_cast<float4*>(sp + e) = v;
         }
-        if (active) {
-            float* sp = a.splat + (size_t)it.w * slot_floats + (my * MT) * slot_ld + mx * MT;
+        // (the next pop's barrier orders these reads before any buffer rewrite)
+    }
+    for (;;) {  // phase 2 (per warp): remainder pieces
+        int w = 0;
+        if (lane == 0) w = ncoop + atomicAdd(&a.totals[kTotQueue2], 1);
+        w = __shfl_sync(0xffffffffu, w, 0);
+        if (w >= nitems) break;
+        const int4 it = a.items[w];
+        const ItemGeo ig = item_geo(a, it, yaxis);
+        float acc[TY][TX];
 #pragma unroll
-            for (int r = 0; r < MT; r++)
+        for (int r = 0; r < TY; r++)
 #pragma unroll
-                for (int c = 0; c < MT; c++) sp[r * slot_ld + c] = acc[r][c];
-        }
+            for (int c = 0; c < TX; c++) acc[r][c] = 0.f;
+        run_chunks<KERN, RADIAL, TY>(acc, a, ig, wbuf, 0, 1, lane);
+        float* sp = a.splat + (size_t)it.w * slot_floats + (my * TY) * S + mx * TX;
+#pragma unroll
+        for (int r = 0; r < TY; r++)
+#pragma unroll
+            for (int c = 0; c < TX; c += 2)
+                *reinterpret_cast<float2*>(sp + r * S + c) = make_float2(acc[r][c], acc[r][c + 1]);
     }
 }
 
@@ -235,32 +275,35 @@ __global__ void __launch_bounds__(256) splat_kernel(const SplatArgs a) {
 // segment blocks are summed IN SEGMENT ORDER into segment 0's slot.  One CTA per
 // (group x sub-window, 1024-float chunk of the slot); float4, 4 segments in flight.
 __global__ void __launch_bounds__(256) segreduce_kernel(const int* __restrict__ hot,
+                                                        const int* __restrict__ totals,
                                                         const int2* __restrict__ group, int nsub,
                                                         int slot_floats, float* __restrict__ splat) {
-    const int gsub = blockIdx.y;
-    const int2 gr = group[hot[gsub / nsub]];
-    const int sub = gsub % nsub;
     const int e = (blockIdx.x * 256 + threadIdx.x) * 4;
     if (e >= slot_floats) return;
-    float* d0 = splat + ((size_t)gr.x * nsub + sub) * slot_floats + e;
+    const int nwork = totals[kTotHot] * nsub;
     const size_t stride = (size_t)nsub * slot_floats;
-    float4 acc = *reinterpret_cast<const float4*>(d0);
-    int k = 1;
-    for (; k + 4 <= gr.y; k += 4) {
-        const float4 v0 = *reinterpret_cast<const float4*>(d0 + k * stride);
-        const float4 v1 = *reinterpret_cast<const float4*>(d0 + (k + 1) * stride);
-        const float4 v2 = *reinterpret_cast<const float4*>(d0 + (k + 2) * stride);
-        const float4 v3 = *reinterpret_cast<const float4*>(d0 + (k + 3) * stride);
-        acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
-        acc.x += v1.x; acc.y += v1.y; acc.z += v1.z; acc.w += v1.w;
-        acc.x += v2.x; acc.y += v2.y; acc.z += v2.z; acc.w += v2.w;
-        acc.x += v3.x; acc.y += v3.y; acc.z += v3.z; acc.w += v3.w;
+    for (int gsub = blockIdx.y; gsub < nwork; gsub += gridDim.y) {
+        const int2 gr = group[hot[gsub / nsub]];
+        const int sub = gsub % nsub;
+        float* d0 = splat + ((size_t)gr.x * nsub + sub) * slot_floats + e;
+        float4 acc = *reinterpret_cast<const float4*>(d0);
+        int k = 1;
+        for (; k + 4 <= gr.y; k += 4) {
+            const float4 v0 = *reinterpret_cast<const float4*>(d0 + k * stride);
+            const float4 v1 = *reinterpret_cast<const float4*>(d0 + (k + 1) * stride);
+            const float4 v2 = *reinterpret_cast<const float4*>(d0 + (k + 2) * stride);
+            const float4 v3 = *reinterpret_cast<const float4*>(d0 + (k + 3) * stride);
+            acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
+            acc.x += v1.x; acc.y += v1.y; acc.z += v1.z; acc.w += v1.w;
+            acc.x += v2.x; acc.y += v2.y; acc.z += v2.z; acc.w += v2.w;
+            acc.x += v3.x; acc.y += v3.y; acc.z += v3.z; acc.w += v3.w;
+        }
+        for (; k < gr.y; k++) {
+            const float4 v = *reinterpret_cast<const float4*>(d0 + k * stride);
+            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+        *reinterpret_cast<float4*>(d0) = acc;
     }
-    for (; k < gr.y; k++) {
-        const float4 v = *reinterpret_cast<const float4*>(d0 + k * stride);
-        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-    }
-    *reinterpret_cast<float4*>(d0) = acc;
 }
 
 // Combine pass: out(i,j) = scale * sum, in order, of the splat blocks covering (i,j).
@@ -370,40 +413,31 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineArgs a) {
     }
 }
 
-template <int K, bool RAD, int MT>
-static void launch_mt(const SplatArgs& a, int grid, int threads, cudaStream_t s) {
-    const size_t smem = sizeof(float) * 2 * kChunk * a.ld;
-    splat_kernel<K, RAD, MT><<<grid, threads, smem, s>>>(a);
-}
-
-template <int K, bool RAD, int MT>
-static int occ_mt(int threads, size_t smem) {
-    int nb = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, splat_kernel<K, RAD, MT>, threads, smem);
-    return nb > 0 ? nb : 1;
-}
-
-template <int K, bool RAD>
-static int launch_one(const SplatArgs& a, int mt, int grid, int threads, cudaStream_t s) {
-    const size_t smem = sizeof(float) * 2 * kChunk * a.ld;
-    if (grid <= 0) {  // query: persistent CTAs per SM
-        switch (mt) {
-        case 3: return occ_mt<K, RAD, 3>(threads, smem);
-        case 4: return occ_mt<K, RAD, 4>(threads, smem);
-        case 5: return occ_mt<K, RAD, 5>(threads, smem);
-        default: return occ_mt<K, RAD, 6>(threads, smem);
-        }
+template <int K, bool RAD, int TY>
+static int launch_ty(const SplatArgs& a, int grid, cudaStream_t s) {
+    const size_t smem = sizeof(float) * WLayout<TY>::SMEM_FLOATS;
+    if (grid <= 0) {  // configure + query: persistent CTAs per SM
+        cudaFuncSetAttribute(splat_kernel<K, RAD, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int nb = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, splat_kernel<K, RAD, TY>, kWarps * 32, smem);
+        return nb > 0 ? nb : 1;
     }
-    switch (mt) {
-    case 3: launch_mt<K, RAD, 3>(a, grid, threads, s); break;
-    case 4: launch_mt<K, RAD, 4>(a, grid, threads, s); break;
-    case 5: launch_mt<K, RAD, 5>(a, grid, threads, s); break;
-    default: launch_mt<K, RAD, 6>(a, grid, threads, s); break;
-    }
+    splat_kernel<K, RAD, TY><<<grid, kWarps * 32, smem, s>>>(a);
     return 0;
 }
 
-using LaunchFn = int (*)(const SplatArgs&, int, int, int, cudaStream_t);
+template <int K, bool RAD>
+static int launch_one(const SplatArgs& a, int ty, int grid, cudaStream_t s) {
+    switch (ty) {
+    case 2: return launch_ty<K, RAD, 2>(a, grid, s);
+    case 3: return launch_ty<K, RAD, 3>(a, grid, s);
+    case 4: return launch_ty<K, RAD, 4>(a, grid, s);
+    case 5: return launch_ty<K, RAD, 5>(a, grid, s);
+    default: return launch_ty<K, RAD, 6>(a, grid, s);
+    }
+}
+
+using LaunchFn = int (*)(const SplatArgs&, int, int, cudaStream_t);
 static const LaunchFn kSplat[2][8] = {
     {launch_one<0, false>, launch_one<1, false>, launch_one<2, false>, launch_one<3, false>,
      launch_one<4, false>, launch_one<5, false>, launch_one<6, false>, launch_one<7, false>},
@@ -422,10 +456,11 @@ KConst make_kconst(double hpx) {
 
 int launch_combine(kde_ctx* c, const EvalPlan& pl, float* out, cudaStream_t s) {
     const Geom& g = c->g;
-    if (pl.nhot > 0) {  // split groups: sum their segments first (fixed order)
+    {   // split groups (count on the device): sum their segments first, in segment order
         const int sf = (int)pl.pg.slot_floats();
-        dim3 grid((sf / 4 + 255) / 256, pl.nhot * pl.pg.nsub());
-        segreduce_kernel<<<grid, 256, 0, s>>>(pl.d_hot, pl.d_group, pl.pg.nsub(), sf, pl.d_splat);
+        const int gx = (sf / 4 + 255) / 256;
+        dim3 grid(gx, std::max(1, 148 * 16 / gx));
+        segreduce_kernel<<<grid, 256, 0, s>>>(pl.d_hot, pl.d_totals, pl.d_group, pl.pg.nsub(), sf, pl.d_splat);
         c->launches += 1;
     }
     CombineArgs a;
@@ -444,38 +479,30 @@ int launch_combine(kde_ctx* c, const EvalPlan& pl, float* out, cudaStream_t s) {
 
 int launch_direct(kde_ctx* c, float* out, cudaStream_t s) {
     EvalPlan& pl = c->plan[KDE_PATH_DIRECT];
-    if (pl.nitems > 0) {
-        SplatArgs a;
-        a.g = c->g;
-        a.offsets = c->d_offsets;
-        a.xy = c->pb.xy;
-        a.rng = c->pb.rng;
-        a.items = pl.d_items;
-        a.group = pl.d_group;
-        a.done = pl.d_done;
-        a.splat = pl.d_splat;
-        a.pg = pl.pg;
-        a.nitems = pl.nitems;
-        a.nslots = pl.nslots;
-        a.k = make_kconst(c->hpx);
-        a.c2 = (float)(c->ceff * c->ceff);
-        a.ld = pl.ld;
-        a.q2 = (float)exp2(2.0 * (double)a.k.kq);
-        a.recur = -(double)a.k.kq * (c->g.R + 8.0) * (c->g.R + 8.0) < 120.0;
-        LaunchFn fn = kSplat[c->radial ? 1 : 0][c->kern];
-        if (pl.grid <= 0) {
-            int nsm = 148;
-            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->p.device);
-            pl.grid = nsm * fn(a, pl.mt, 0, pl.threads, s);
-        }
-        // arrival counters + queue head (done[nslots]) start at zero
-        cudaMemsetAsync(pl.d_done, 0, sizeof(int) * ((size_t)pl.nslots + 1), s);
-        tmark(c, 3, s);
-        fn(a, pl.mt, pl.nitems < pl.grid ? pl.nitems : pl.grid, pl.threads, s);
-        c->launches += 1;
-    } else {
-        tmark(c, 3, s);
+    SplatArgs a;
+    a.g = c->g;
+    a.offsets = c->d_offsets;
+    a.xy = c->pb.xy;
+    a.rng = c->pb.rng;
+    a.items = pl.d_items;
+    a.group = pl.d_group;
+    a.totals = pl.d_totals;
+    a.splat = pl.d_splat;
+    a.pg = pl.pg;
+    a.k = make_kconst(c->hpx);
+    a.c2 = (float)(c->ceff * c->ceff);
+    a.q2 = (float)exp2(2.0 * (double)a.k.kq);
+    a.recur = -(double)a.k.kq * (c->g.R + 8.0) * (c->g.R + 8.0) < 120.0;
+    LaunchFn fn = kSplat[c->radial ? 1 : 0][c->kern];
+    if (pl.grid <= 0) {
+        int nsm = 148;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->p.device);
+        pl.grid = nsm * fn(a, pl.mt, 0, s);
     }
+    cudaMemsetAsync(pl.d_totals + kTotQueue, 0, 2 * sizeof(int), s);  // work-queue heads
+    tmark(c, 3, s);
+    fn(a, pl.mt, pl.grid, s);  // persistent; the item count is on the device
+    c->launches += 1;
     tmark(c, 4, s);
     launch_combine(c, pl, out, s);
     tmark(c, 5, s);

@@ -43,9 +43,8 @@ struct TcArgs {
     const uint2* __restrict__ rng;
     const int4* __restrict__ items;
     const int2* __restrict__ group;
-    int* __restrict__ done;
+    int* __restrict__ totals;  // plan totals (kTot*): item count, work-queue head
     float* __restrict__ splat;
-    int nitems, nslots;
     int n;          // MMA N
     int tmem_cols;  // allocated TMEM columns (power of two >= n)
     float kq, q2;   // Gaussian: -log2(e)/(2 h^2), 2^(2 kq)
@@ -197,14 +196,15 @@ __global__ void __launch_bounds__(kTcThreads, 8) tc_splat_kernel(const TcArgs a)
     const uint32_t sm_b = sm_a + 2 * kTcABytes;             // B buffer b at sm_b + b * bbytes
     const uint32_t koff = (uint32_t)((lane >> 3) * 128 + (lane & 7) * 16);  // point = k index
     const int nbu = a.n / 8;                                // B column units
-    if (t == 0) s_w = atomicAdd(&a.done[a.nslots], 1);
+    const int nitems = a.totals[kTotSlots];
+    if (t == 0) s_w = atomicAdd(&a.totals[kTotQueue], 1);
     for (;;) {
         __syncthreads();
         const int w = s_w;
-        if (w >= a.nitems) break;
+        if (w >= nitems) break;
         const int4 it = a.items[w];
-        __syncthreads();                                    // everyone has read s_w
-        if (t == 0) s_w = atomicAdd(&a.done[a.nslots], 1);  // pop the next item early
+        __syncthreads();                                         // everyone has read s_w
+        if (t == 0) s_w = atomicAdd(&a.totals[kTotQueue], 1);  // pop the next item early
         const int gx = it.x % pg.ngx, gy = it.x / pg.ngx;
         const int ox = gx * pg.px - g.F, oy = gy * pg.py - g.F;  // window origin (pixels)
         // the stack's buckets are the contiguous keys gx*nby + gy*s + k (column-major keys):
@@ -305,49 +305,43 @@ __global__ void __launch_bounds__(kTcThreads, 8) tc_splat_kernel(const TcArgs a)
 
 int launch_tc(kde_ctx* c, float* out, cudaStream_t s) {
     EvalPlan& pl = c->plan[KDE_PATH_TENSOR];
-    if (pl.nitems > 0) {
-        TcArgs a;
-        a.g = c->g;
-        a.pg = pl.pg;
-        a.offsets = c->d_offsets;
-        a.xy = c->pb.xy;
-        a.rng = c->pb.rng;
-        a.items = pl.d_items;
-        a.group = pl.d_group;
-        a.done = pl.d_done;
-        a.splat = pl.d_splat;
-        a.nitems = pl.nitems;
-        a.nslots = pl.nslots;
-        a.n = pl.pg.slot_w;
-        a.tmem_cols = 32;
-        while (a.tmem_cols < a.n) a.tmem_cols <<= 1;
-        a.kq = (float)(-0.5 * 1.4426950408889634074 / (c->hpx * c->hpx));
-        a.q2 = (float)exp2(2.0 * (double)a.kq);
-        const size_t smem = 2 * (size_t)kTcABytes + 2 * (size_t)a.n * kTcChunk * 2 + 1024;
-        if (pl.grid <= 0) {
-            cudaFuncSetAttribute(tc_splat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            int nsm = 148, per = 0;
-            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->p.device);
-            const cudaError_t oe =
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tc_splat_kernel, kTcThreads, smem);
-            if (getenv("KDE_DEBUG"))
-                fprintf(stderr, "[kde] tc occupancy query: err=%d per=%d smem=%zu\n", (int)oe, per, smem);
-            // (the occupancy API reports 1 CTA/SM for this kernel; size from the real limits:
-            //  shared memory, and TMEM columns below)
-            if (oe != cudaSuccess) cudaGetLastError();
-            per = std::max(per, (int)((200u << 10) / (smem + 2048)));
-            // persistent CTAs hold their TMEM allocation for the whole launch: never
-            // oversubscribe the 512 columns of an SM
-            per = std::max(1, std::min(per, 512 / a.tmem_cols));
-            pl.grid = nsm * per;
-        }
-        cudaMemsetAsync(pl.d_done, 0, sizeof(int) * ((size_t)pl.nslots + 1), s);
-        tmark(c, 3, s);
-        tc_splat_kernel<<<std::min(pl.grid, pl.nitems), kTcThreads, smem, s>>>(a);
-        c->launches += 1;
-    } else {
-        tmark(c, 3, s);
+    TcArgs a;
+    a.g = c->g;
+    a.pg = pl.pg;
+    a.offsets = c->d_offsets;
+    a.xy = c->pb.xy;
+    a.rng = c->pb.rng;
+    a.items = pl.d_items;
+    a.group = pl.d_group;
+    a.totals = pl.d_totals;
+    a.splat = pl.d_splat;
+    a.n = pl.pg.slot_w;
+    a.tmem_cols = 32;
+    while (a.tmem_cols < a.n) a.tmem_cols <<= 1;
+    a.kq = (float)(-0.5 * 1.4426950408889634074 / (c->hpx * c->hpx));
+    a.q2 = (float)exp2(2.0 * (double)a.kq);
+    const size_t smem = 2 * (size_t)kTcABytes + 2 * (size_t)a.n * kTcChunk * 2 + 1024;
+    if (pl.grid <= 0) {
+        cudaFuncSetAttribute(tc_splat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int nsm = 148, per = 0;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->p.device);
+        const cudaError_t oe =
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tc_splat_kernel, kTcThreads, smem);
+        if (getenv("KDE_DEBUG"))
+            fprintf(stderr, "[kde] tc occupancy query: err=%d per=%d smem=%zu\n", (int)oe, per, smem);
+        // (the occupancy API reports 1 CTA/SM for this kernel; size from the real limits:
+        //  shared memory, and TMEM columns below)
+        if (oe != cudaSuccess) cudaGetLastError();
+        per = std::max(per, (int)((200u << 10) / (smem + 2048)));
+        // persistent CTAs hold their TMEM allocation for the whole launch: never
+        // oversubscribe the 512 columns of an SM
+        per = std::max(1, std::min(per, 512 / a.tmem_cols));
+        pl.grid = nsm * per;
     }
+    cudaMemsetAsync(pl.d_totals + kTotQueue, 0, sizeof(int), s);  // work-queue head
+    tmark(c, 3, s);
+    tc_splat_kernel<<<pl.grid, kTcThreads, smem, s>>>(a);  // persistent; item count on device
+    c->launches += 1;
     tmark(c, 4, s);
     launch_combine(c, pl, out, s);
     tmark(c, 5, s);

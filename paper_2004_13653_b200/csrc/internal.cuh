@@ -12,10 +12,11 @@
 
 namespace kde {
 
-constexpr int kSub = 64;          // splat sub-window edge (pixels): one CTA, <= 256 threads
+constexpr int kSubMax = 48;       // direct-path sub-window edge bound (pixels): S = 8 TY <= 48
 constexpr int kSegPts = 512;      // split-K: points per splat work item (a constant, so the
                                   // plan is invariant under band sharding);
                                   // also bounds every fp32 running sum to 512 terms (R10)
+constexpr int kPartPtsDirect = 128;  // direct path: remainder piece = one warp's work item
 constexpr int kCombTile = 32;     // combine-pass output tile edge
 constexpr int kTcM = 128;         // tensor-core tile rows = TMEM lanes
 
@@ -60,6 +61,8 @@ struct PathGeom {
     int nsubx = 1, nsuby = 1;
     int sx = 0, sy = 0;
     int slot_w = 0, slot_h = 0;
+    int part_pts = kSegPts;  // a group's remainder (< kSegPts points) is cut into pieces of
+                             // <= part_pts points, one work item each (direct: 128, one warp)
     __host__ __device__ int nsub() const { return nsubx * nsuby; }
     __host__ __device__ int ngroups() const { return ngx * ngy; }
     __host__ __device__ int64_t slot_floats() const { return (int64_t)slot_w * slot_h; }
@@ -69,25 +72,41 @@ struct EvalPlan {
     PathGeom pg;
     bool enabled = false;
     // SIMT splat launch shape (direct path)
-    int mt = 4;                                // register micro-tile edge
-    int ld = 8;                                // factor row stride (floats)
-    int threads = 32;                          // CTA size
-    int grid = 0, grid_key = -1;               // persistent grid (0: not yet queried)
-    // per-load totals (read back once)
-    int tf = 0, tp = 0, nslots = 0, nitems = 0;
-    // device buffers
+    int mt = 4;                                // lane tile rows TY (columns 2 TY), S = 8 TY
+    int grid = 0;                              // persistent grid (0: not yet queried)
+    int64_t planned_gen = -1;                  // load generation this plan belongs to
+    // device buffers.  The plan's sizes stay on the device (kTot*): kernels read them, the
+    // host never waits for them (buffers are reserved at their upper bounds).
     uint64_t* d_local = nullptr;               // block-local prefixes (full << 32 | part)
     uint64_t* d_bsum = nullptr;                // block totals -> their exclusive scan
     int2* d_group = nullptr;                   // per group: (first segment, #segments)
-    int* d_totals = nullptr;                   // TF, TP, nslots, n_binned, #hot groups
+    int* d_totals = nullptr;                   // see kTot*
     int* d_hot = nullptr;                      // groups with > 1 segment (segment reduce)
-    int nhot = 0;
     int4* d_items = nullptr;                   // (group, k0, k1, slot)
     int64_t items_cap = 0;
     float* d_splat = nullptr;
-    int* d_done = nullptr;                     // per slot arrivals (segment reduce); [nslots] = queue
     int64_t slots_cap = 0;
 };
+
+// d_totals layout (ints)
+constexpr int kTotFull = 0;    // full segments
+constexpr int kTotPart = 1;    // partial segments
+constexpr int kTotSlots = 2;   // slots = work items = (full + partial) * nsub
+constexpr int kTotBinned = 3;  // points binned
+constexpr int kTotHot = 4;     // split groups (segment reduce list length)
+constexpr int kTotChunks = 5;  // tensor-core path: 32-point MMA chunks (executed-flop count)
+constexpr int kTotQueue = 6;   // persistent-kernel work-queue head (CTA items)
+constexpr int kTotQueue2 = 7;  // second queue head (direct path: per-warp items)
+constexpr int kTotInts = 8;
+
+// Upper bound on a path's items/slots for n points: every full segment, plus per
+// non-empty group its remainder pieces (at most n / part_pts + one per group), times the
+// sub-windows.
+inline int64_t slot_bound(const PathGeom& pg, int64_t n) {
+    const int64_t ng = (int64_t)pg.ngroups();
+    const int64_t rem = pg.part_pts < kSegPts ? n / pg.part_pts : 0;
+    return (n / kSegPts + rem + (n < ng ? n : ng)) * pg.nsub();
+}
 
 }  // namespace kde
 
@@ -105,13 +124,17 @@ struct kde_ctx {
     cudaEvent_t evald_ev = nullptr;            // end of the last eval (the next load's
                                                // binning waits on it: eval reads the bins)
     cudaEvent_t input_ev = nullptr;            // legacy-stream point for device inputs
+    cudaEvent_t stats_ev = nullptr;            // the load's stats readback has landed
     bool evaluated = false;
-    int* h_totals = nullptr;                   // pinned: plan totals + stats readback
+    int* h_totals = nullptr;                   // pinned: stats readback (asynchronous)
+    bool stats_pending = false;                // h_totals not yet folded into stats
+    size_t splat_budget = 0;                   // max bytes a splat buffer may reserve unread
     kde_stats stats{};
     bool loaded = false;
+    int64_t load_gen = 0;                      // bumped by every load (lazy per-path plans)
     int64_t launches = 0;                      // kernels launched (kde_stats.kernel_launches)
     bool timing = false;                       // record phase events (kde_set_timing)
-    cudaEvent_t tev[6] = {};                   // bin0, bin1/plan0, plan1, main0, main1, comb1
+    cudaEvent_t tev[6] = {};                   // bin0, bin1 (load); plan0, main0, main1, comb1 (eval)
     bool tev_load = false, tev_eval = false;
     kde::EvalPlan plan[2];                     // [KDE_PATH_DIRECT], [KDE_PATH_TENSOR]
 };
@@ -130,7 +153,7 @@ int bin_points(kde_ctx* c, const double* d_x, const double* d_y, int64_t n);
 int launch_direct(kde_ctx* c, float* out, cudaStream_t s);
 int launch_tc(kde_ctx* c, float* out, cudaStream_t s);
 // planning (plan.cu)
-int plan_device(kde_ctx* c, EvalPlan& pl);
+int plan_device(kde_ctx* c, EvalPlan& pl, cudaStream_t s);
 int plan_nblk(const PathGeom& pg);
 int launch_combine(kde_ctx* c, const EvalPlan& pl, float* out, cudaStream_t s);
 

@@ -1,13 +1,16 @@
-// Device-side evaluation plan, three kernels per path and no host round
-// trip except one 16-byte read of the totals (for the splat-buffer capacity).  A path's
-// group is a vertical stack of pg.s buckets (1 for the direct path).
+// Device-side evaluation plan, three kernels per path, built lazily by the
+// first kde_eval of a path after a load, and no host round trip: the totals stay on the
+// device (kTot* in internal.cuh) and the buffers are reserved at their upper bounds.  A
+// path's group is a vertical stack of pg.s buckets (1 for the direct path).
 //
 //   plan_local    per group g whose window meets the band: cnt_g = sum of its buckets'
-//                 counts, full_g = cnt_g / kSegPts full segments, part_g = [cnt_g % kSegPts];
+//                 counts, full_g = cnt_g / kSegPts full segments, part_g =
+//                 ceil((cnt_g % kSegPts) / pg.part_pts) remainder pieces;
 //                 block-local exclusive scan of the packed pair (full_g << 32 | part_g)
 //   plan_blocks   one CTA: exclusive scan of the block totals
 //   plan_finish   global prefixes -> group[g] = (first segment, #segments), the item list
-//                 (all full segments first -- equal work -- then the partial ones;
+//                 (all full segments first -- equal work -- then the remainder pieces of
+//                 <= pg.part_pts points, segment = full segment or remainder piece;
 //                 item = (g, k0, k1, slot), slot = (first segment + seg)*nsub + sub, [k0, k1)
 //                 positions in the concatenation of the group's bucket ranges) and totals
 //
@@ -39,7 +42,8 @@ __device__ __forceinline__ uint64_t group_pair(const Geom& g, const PathGeom& pg
     if (wy1 < g.rb || wy0 > g.re - 1) return 0;  // window misses the band
     const uint32_t c = group_count(g, pg, off, gx, gy);
     *cnt = c;
-    return ((uint64_t)(c / kSegPts) << 32) | (uint64_t)((c % kSegPts) ? 1u : 0u);
+    const uint32_t rem = c % kSegPts;
+    return ((uint64_t)(c / kSegPts) << 32) | (uint64_t)((rem + pg.part_pts - 1) / pg.part_pts);
 }
 
 // block-wide exclusive scan of one u64 per thread (kPlanThreads threads); returns the total
@@ -114,6 +118,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_finish_kernel(
     const int nsub = pg.nsub(), ng = pg.ngroups();
     const int i0 = blockIdx.x * kPlanTile + threadIdx.x * kPlanPer;
     const uint64_t base = bsum[blockIdx.x];
+    uint32_t chunks = 0;  // 32-point chunks of this thread's groups (tensor-core flop count)
 #pragma unroll
     for (int k = 0; k < kPlanPer; k++) {
         const int i = i0 + k;
@@ -125,32 +130,36 @@ __global__ void __launch_bounds__(kPlanThreads) plan_finish_kernel(
         const int nf = (int)(own >> 32), np = (int)(own & 0xffffffffu);
         const int sb = fs + ps;  // first segment (segments numbered group by group)
         group[i] = make_int2(sb, nf + np);
-        if (nf + np > 1) hot[atomicAdd(&totals[4], 1)] = i;  // split group: segment reduce
+        if (nf + np > 1) hot[atomicAdd(&totals[kTotHot], 1)] = i;  // split group: segment reduce
         for (int sg = 0; sg < nf; sg++)
             for (int sub = 0; sub < nsub; sub++)
                 items[(fs + sg) * nsub + sub] =
                     make_int4(i, sg * kSegPts, (sg + 1) * kSegPts, (sb + sg) * nsub + sub);
-        if (np)
+        for (int k = 0; k < np; k++) {  // the remainder's pieces of <= part_pts points
+            const int k0 = nf * kSegPts + k * pg.part_pts, k1 = min(k0 + pg.part_pts, (int)cnt);
             for (int sub = 0; sub < nsub; sub++)
-                items[(TF + ps) * nsub + sub] = make_int4(i, nf * kSegPts, (int)cnt, (sb + nf) * nsub + sub);
+                items[(TF + ps + k) * nsub + sub] = make_int4(i, k0, k1, (sb + nf + k) * nsub + sub);
+        }
+        chunks += (uint32_t)nf * (kSegPts / 32) + ((cnt % kSegPts) + 31) / 32;
     }
+    chunks = __reduce_add_sync(0xffffffffu, chunks);
+    if ((threadIdx.x & 31) == 0 && chunks) atomicAdd(&totals[kTotChunks], (int)chunks);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        totals[0] = TF;                 // full segments
-        totals[1] = TP;                 // partial segments
-        totals[2] = (TF + TP) * nsub;   // slots
-        totals[3] = (int)off[g.nbx * g.nby];  // points binned
+        totals[kTotFull] = TF;
+        totals[kTotPart] = TP;
+        totals[kTotSlots] = (TF + TP) * nsub;
+        totals[kTotBinned] = (int)off[g.nbx * g.nby];
     }
 }
 
 int plan_nblk(const PathGeom& pg) { return (pg.ngroups() + 1 + kPlanTile - 1) / kPlanTile; }
 
-// Enqueue the three plan kernels of one path on the context stream; the item list must
-// already have its upper-bound capacity; totals land in pl.d_totals.
-int plan_device(kde_ctx* c, EvalPlan& pl) {
+// Enqueue the three plan kernels of one path on stream s; the item list must already have
+// its upper-bound capacity; totals land in pl.d_totals.
+int plan_device(kde_ctx* c, EvalPlan& pl, cudaStream_t s) {
     const PathGeom& pg = pl.pg;
     const int nblk = plan_nblk(pg);
-    cudaStream_t s = c->stream;
-    cudaMemsetAsync(pl.d_totals + 4, 0, sizeof(int), s);  // hot-group counter
+    cudaMemsetAsync(pl.d_totals, 0, sizeof(int) * kTotInts, s);  // counters start at zero
     plan_local_kernel<<<nblk, kPlanThreads, 0, s>>>(c->g, pg, c->d_offsets, pl.d_local, pl.d_bsum);
     plan_blocks_kernel<<<1, kPlanThreads, 0, s>>>(pl.d_bsum, nblk);
     plan_finish_kernel<<<nblk, kPlanThreads, 0, s>>>(c->g, pg, c->d_offsets, pl.d_local, pl.d_bsum,
