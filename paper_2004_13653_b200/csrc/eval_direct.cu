@@ -90,21 +90,24 @@ __device__ __forceinline__ void lds_n(const float* p, float* v) {
 
 // The 8 units of TY factors of one point along one axis: unit u covers sub-window
 // coordinates c = u*TY + e; f = [c in range] * khat(c + 1/2 - P), ph = P - 1/2 in
-// sub-window coordinates, [lo, lo + span] the point's integer range along the axis.
-// The Gaussian uses the exact-ratio recurrence g(d+1) = g(d) r(d), r(d+1) = r(d) 2^(2kq)
-// (2 FMUL per factor, reseeded per unit); radial forms store s^2 (or +inf when masked).
-template <int KERN, bool RADIAL, int TY>
-__device__ __forceinline__ void factor_axis(float* dst_pt, bool yaxis, float ph, int lo, int span,
+// sub-window coordinates, [lo, hi] the point's integer range along the axis (as a 64-bit
+// mask over the 8 TY <= 48 coordinates).  The Gaussian uses the exact-ratio recurrence
+// g(d+1) = g(d) r(d), r(d+1) = r(d) 2^(2kq) (2 FMUL per factor, reseeded per unit);
+// radial forms store s^2 (or +inf when masked).
+template <int KERN, bool RADIAL, int TY, bool RECUR>
+__device__ __forceinline__ void factor_axis(float* dst_pt, bool yaxis, float ph, int lo, int hi,
                                             const SplatArgs& a) {
     using L = WLayout<TY>;
+    // bits lo..hi of the sub-window coordinates (clipped to [0, 64))
+    const int l = max(lo, 0), h = min(hi, 63);
+    const uint64_t m64 = (l <= h) ? ((~0ull >> (63 - h)) & (~0ull << l)) : 0ull;
 #pragma unroll
     for (int u = 0; u < 8; u++) {
         const int c0 = u * TY;
-        const int l0 = max(lo - c0, 0), h0 = min(lo + span - c0, TY - 1);
-        const uint32_t m = (l0 <= h0) ? ((2u << h0) - (1u << l0)) : 0u;
+        const uint32_t m = (uint32_t)(m64 >> c0);
         const float d0 = (float)c0 - ph;
         float f[TY];
-        if (!RADIAL && KERN == 6 && a.recur) {
+        if constexpr (RECUR) {
             float gv = ex2_ftz(d0 * d0 * a.k.kq);
             float r = ex2_ftz(fmaf(2.0f, d0, 1.0f) * a.k.kq);
 #pragma unroll
@@ -152,8 +155,9 @@ __device__ __forceinline__ ItemGeo item_geo(const SplatArgs& a, const int4& it, 
 }
 
 // Accumulate chunks ch0, ch0 + step, ... of an item into the lane's register tile, using
-// this warp's factor buffer wbuf (warp-synchronous; no CTA barrier).
-template <int KERN, bool RADIAL, int TY>
+// this warp's factor buffer wbuf (warp-synchronous; no CTA barrier).  The next chunk's
+// point is loaded while the current one is evaluated.
+template <int KERN, bool RADIAL, int TY, bool RECUR>
 __device__ __forceinline__ void run_chunks(float (&acc)[TY][2 * TY], const SplatArgs& a, const ItemGeo& ig,
                                            float* wbuf, int ch0, int step, int lane) {
     using L = WLayout<TY>;
@@ -164,15 +168,33 @@ __device__ __forceinline__ void run_chunks(float (&acc)[TY][2 * TY], const Splat
     const int nch = (ig.cnt + kWChunk - 1) / kWChunk;
     const float* fxp = wbuf + mx * L::TXP;
     const float* fyp = wbuf + L::rowoff(my);
-    for (int ch = ch0; ch < nch; ch += step) {
-        const int q = ch * kWChunk + gp;
-        if (q < ig.cnt) {  // 1-D factors of point q along this lane's axis
+    float npos = 0.f;
+    uint32_t nrg = 1u;  // lo = 1 > hi = 0: empty
+    {
+        const int q = ch0 * kWChunk + gp;
+        if (ch0 < nch && q < ig.cnt) {
             const float2 l = a.xy[ig.base + q];
             const uint2 rr = a.rng[ig.base + q];
-            const uint32_t pr = yaxis ? rr.y : rr.x;
-            const int lo = (int)(pr & 0xffffu) - ig.oo, hi = (int)(pr >> 16) - ig.oo;
-            factor_axis<KERN, RADIAL, TY>(wbuf + gp * L::LDP, yaxis, (yaxis ? l.y : l.x) + ig.sh, lo, hi - lo, a);
+            npos = yaxis ? l.y : l.x;
+            nrg = yaxis ? rr.y : rr.x;
         }
+    }
+    for (int ch = ch0; ch < nch; ch += step) {
+        const float pos = npos;
+        const uint32_t pr = nrg;
+        const bool valid = ch * kWChunk + gp < ig.cnt;
+        {   // prefetch the next chunk's point
+            const int q = (ch + step) * kWChunk + gp;
+            if (q < ig.cnt) {
+                const float2 l = a.xy[ig.base + q];
+                const uint2 rr = a.rng[ig.base + q];
+                npos = yaxis ? l.y : l.x;
+                nrg = yaxis ? rr.y : rr.x;
+            }
+        }
+        if (valid)  // 1-D factors of this lane's point along its axis
+            factor_axis<KERN, RADIAL, TY, RECUR>(wbuf + gp * L::LDP, yaxis, pos + ig.sh,
+                                                 (int)(pr & 0xffffu) - ig.oo, (int)(pr >> 16) - ig.oo, a);
         __syncwarp();
         const int np = min(kWChunk, ig.cnt - ch * kWChunk);
 #pragma unroll 2
@@ -199,7 +221,7 @@ __device__ __forceinline__ void run_chunks(float (&acc)[TY][2 * TY], const Splat
 // Splat pass.  Phase 1: the CTA's 8 warps share each full segment (warp w takes chunks
 // w, w+8, ...; tiles summed in warp order through shared memory).  Phase 2: every warp
 // alone pops remainder pieces (<= 128 points) and writes its tile straight to the slot.
-template <int KERN, bool RADIAL, int TY>
+template <int KERN, bool RADIAL, int TY, bool RECUR>
 __global__ void __launch_bounds__(kWarps * 32, 2) splat_kernel(const SplatArgs a) {
     using L = WLayout<TY>;
     constexpr int TX = L::TX, S = L::S;
@@ -226,7 +248,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) splat_kernel(const SplatArgs a
         for (int r = 0; r < TY; r++)
 #pragma unroll
             for (int c = 0; c < TX; c++) acc[r][c] = 0.f;
-        run_chunks<KERN, RADIAL, TY>(acc, a, ig, wbuf, warp, kWarps, lane);
+        run_chunks<KERN, RADIAL, TY, RECUR>(acc, a, ig, wbuf, warp, kWarps, lane);
         __syncthreads();  // every warp is done with its factor buffer
         {
             float* red = smem + warp * (S * S) + (my * TY) * S + mx * TX;
@@ -261,7 +283,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) splat_kernel(const SplatArgs a
         for (int r = 0; r < TY; r++)
 #pragma unroll
             for (int c = 0; c < TX; c++) acc[r][c] = 0.f;
-        run_chunks<KERN, RADIAL, TY>(acc, a, ig, wbuf, 0, 1, lane);
+        run_chunks<KERN, RADIAL, TY, RECUR>(acc, a, ig, wbuf, 0, 1, lane);
         float* sp = a.splat + (size_t)it.w * slot_floats + (my * TY) * S + mx * TX;
 #pragma unroll
         for (int r = 0; r < TY; r++)
@@ -413,17 +435,25 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineArgs a) {
     }
 }
 
-template <int K, bool RAD, int TY>
+template <int K, bool RAD, int TY, bool REC>
 static int launch_ty(const SplatArgs& a, int grid, cudaStream_t s) {
     const size_t smem = sizeof(float) * WLayout<TY>::SMEM_FLOATS;
     if (grid <= 0) {  // configure + query: persistent CTAs per SM
-        cudaFuncSetAttribute(splat_kernel<K, RAD, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(splat_kernel<K, RAD, TY, REC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int nb = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, splat_kernel<K, RAD, TY>, kWarps * 32, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, splat_kernel<K, RAD, TY, REC>, kWarps * 32, smem);
         return nb > 0 ? nb : 1;
     }
-    splat_kernel<K, RAD, TY><<<grid, kWarps * 32, smem, s>>>(a);
+    splat_kernel<K, RAD, TY, REC><<<grid, kWarps * 32, smem, s>>>(a);
     return 0;
+}
+
+template <int K, bool RAD, int TY>
+static int launch_ty(const SplatArgs& a, int grid, cudaStream_t s) {
+    // the Gaussian's exact-ratio recurrence, when its range stays normal (a.recur)
+    if constexpr (K == 6 && !RAD)
+        if (a.recur) return launch_ty<K, RAD, TY, true>(a, grid, s);
+    return launch_ty<K, RAD, TY, false>(a, grid, s);
 }
 
 template <int K, bool RAD>
