@@ -562,6 +562,7 @@ void kde_free(kde_ctx* c) {
     }
     cudaFree(pb.hist);
     cudaFree(pb.scan_tmp);
+    cudaFree(pb.rec);
     cudaFree(pb.xy);
     cudaFree(pb.rng);
     cudaFree(c->d_offsets);

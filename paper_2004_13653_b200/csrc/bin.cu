@@ -63,40 +63,57 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
     return v;
 }
 
-// a1 kernel: keys + integer stats (n_finite, n_outside, useful_pairs).
-__global__ void __launch_bounds__(256) bin_convert_kernel(const double* __restrict__ x,
-                                                          const double* __restrict__ y, int n,
-                                                          Geom g, uint32_t sentinel,
-                                                          uint32_t* __restrict__ key,
-                                                          unsigned long long* __restrict__ stats) {
+// ---------------------------------------------------------------------------------
+// a2 constants (the convert kernel below already works in sort tiles)
+constexpr int kRsThreads = 256;
+constexpr int kRsMaxBits = 11;
+// A sort tile is kRsThreads x rounds keys, rounds = max(8, nbins / 64): tiles hold at least
+// 4 keys per digit, so the per-tile histograms stay <= 1/4 of the keys.
+inline int rs_rounds(int nbins) { return nbins / 64 > 8 ? nbins / 64 : 8; }
+
+// a1 kernel, one sort tile (kRsThreads x rounds points) per CTA: keys, the point's record (bucket-
+// local fp32 coordinates + packed int16 ranges, read back by the gather), the integer
+// stats (n_finite, n_outside, useful_pairs) and the tile's histogram of the first radix
+// digit (the first pass's upsweep, fused).
+__global__ void __launch_bounds__(kRsThreads, 4) bin_convert_kernel(
+    const double* __restrict__ x, const double* __restrict__ y, int n, Geom g, uint32_t sentinel,
+    uint32_t* __restrict__ key, uint4* __restrict__ rec, unsigned long long* __restrict__ stats,
+    uint32_t dmask, uint32_t* __restrict__ hist, int nblk, int rounds) {
+    extern __shared__ uint32_t h[];  // [dmask + 1]
+    const int nbins = (int)dmask + 1;
+    for (int d = threadIdx.x; d < nbins; d += kRsThreads) h[d] = 0;
     unsigned long long nf = 0, no = 0, up = 0;
     const int rb = g.rb, re = g.re;
-    constexpr int U = 4;  // points per thread per iteration: loads issued before use
-    const int tile = blockDim.x * U;
-    for (int i0 = blockIdx.x * tile + threadIdx.x; i0 < n; i0 += gridDim.x * tile) {
-        double xv[U], yv[U];
+    const int base = blockIdx.x * kRsThreads * rounds + threadIdx.x;
+    __syncthreads();
+    constexpr int kHalf = 4;  // batches of loads-then-compute
+    for (int hb = 0; hb < rounds / kHalf; hb++) {
+        double xv[kHalf], yv[kHalf];
 #pragma unroll
-        for (int u = 0; u < U; u++) {
-            const int i = i0 + u * blockDim.x;
-            xv[u] = i < n ? x[i] : 0.0;
-            yv[u] = i < n ? y[i] : 0.0;
+        for (int r = 0; r < kHalf; r++) {
+            const int i = base + (hb * kHalf + r) * kRsThreads;
+            xv[r] = i < n ? x[i] : 0.0;
+            yv[r] = i < n ? y[i] : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < U; u++) {
-            const int i = i0 + u * blockDim.x;
+        for (int r = 0; r < kHalf; r++) {
+            const int i = base + (hb * kHalf + r) * kRsThreads;
             if (i >= n) break;
-            const Binned b = bin_point(xv[u], yv[u], g, sentinel);
+            const Binned b = bin_point(xv[r], yv[r], g, sentinel);
             key[i] = b.key;
+            rec[i] = make_uint4(__float_as_uint(b.lx), __float_as_uint(b.ly),
+                                ((uint32_t)b.ilo & 0xffffu) | ((uint32_t)b.ihi << 16),
+                                ((uint32_t)b.jlo & 0xffffu) | ((uint32_t)b.jhi << 16));
+            atomicAdd(&h[b.key & dmask], 1u);
             nf += b.status > 0;
             no += b.status == 1;
             if (b.status == 2) {
                 const int jl = max(b.jlo, rb), jh = min(b.jhi, re - 1);
-                if (jh >= jl)
-                    up += (unsigned long long)(b.ihi - b.ilo + 1) * (unsigned long long)(jh - jl + 1);
+                if (jh >= jl) up += (unsigned long long)(b.ihi - b.ilo + 1) * (unsigned long long)(jh - jl + 1);
             }
         }
     }
-    __shared__ unsigned long long s[3][8];
+    __shared__ unsigned long long s[3][kRsThreads / 32];
     nf = warp_sum_u64(nf);
     no = warp_sum_u64(no);
     up = warp_sum_u64(up);
@@ -109,32 +126,30 @@ __global__ void __launch_bounds__(256) bin_convert_kernel(const double* __restri
     __syncthreads();
     if (threadIdx.x < 3) {
         unsigned long long t = 0;
-        for (int k = 0; k < (int)(blockDim.x >> 5); k++) t += s[threadIdx.x][k];
+        for (int k = 0; k < kRsThreads / 32; k++) t += s[threadIdx.x][k];
         if (t) atomicAdd(&stats[threadIdx.x], t);
     }
+    for (int d = threadIdx.x; d < nbins; d += kRsThreads) hist[(size_t)d * nblk + blockIdx.x] = h[d];
 }
 
 // ---------------------------------------------------------------------------------
 // a2: stable LSD counting sort.  Keys lie in [0, nb] (nb = dropped); passes =
 // ceil(bits/11) with digits of ceil(bits/passes) <= 11 bits (two passes up to 2^22
-// buckets).  Per pass: per-block digit histograms -> exclusive scan (digit-major) ->
-// stable in-block ranking (warp match_any; per-warp digit counts; leaders only clear what
-// they set) + scatter.
-constexpr int kRsThreads = 256;
-constexpr int kRsRounds = 8;
-constexpr int kRsChunk = kRsThreads * kRsRounds;
-constexpr int kRsMaxBits = 11;
+// buckets).  Per pass: per-tile digit histograms (pass 0: fused into the convert
+// kernel) -> per-digit exclusive scan over the tiles + digit totals (one kernel) ->
+// stable in-tile ranking (warp match_any; per-warp digit counts; leaders only clear what
+// they set) + scatter, each tile adding the exclusive scan of the digit totals.
 
 __global__ void __launch_bounds__(kRsThreads) rs_upsweep(const uint32_t* __restrict__ keys, int n,
                                                          int shift, uint32_t dmask,
-                                                         uint32_t* __restrict__ hist, int nblk) {
+                                                         uint32_t* __restrict__ hist, int nblk, int rounds) {
     extern __shared__ uint32_t h[];  // [dmask + 1]
     const int nbins = (int)dmask + 1;
     for (int d = threadIdx.x; d < nbins; d += kRsThreads) h[d] = 0;
     __syncthreads();
-    const int base = blockIdx.x * kRsChunk;
-#pragma unroll
-    for (int r = 0; r < kRsRounds; r++) {
+    const int base = blockIdx.x * kRsThreads * rounds;
+#pragma unroll 8
+    for (int r = 0; r < rounds; r++) {
         const int i = base + r * kRsThreads + threadIdx.x;
         if (i < n) atomicAdd(&h[(keys[i] >> shift) & dmask], 1u);
     }
@@ -145,22 +160,45 @@ __global__ void __launch_bounds__(kRsThreads) rs_upsweep(const uint32_t* __restr
 __global__ void __launch_bounds__(kRsThreads) rs_downsweep(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
     uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, int n, int shift, uint32_t dmask,
-    const uint32_t* __restrict__ hscan, int nblk) {
+    const uint32_t* __restrict__ hscan, const uint32_t* __restrict__ dtot, int nblk, int rounds) {
     extern __shared__ uint32_t sm[];
     const int nbins = (int)dmask + 1;
     uint32_t* run = sm;                                   // [nbins] running count per digit
     uint32_t* boff = sm + nbins;                          // [nbins] block base per digit
     uint16_t* wcnt = reinterpret_cast<uint16_t*>(sm + 2 * nbins);  // [8][nbins]
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-    for (int d = t; d < nbins; d += kRsThreads) {
-        run[d] = 0;
-        boff[d] = hscan[(size_t)d * nblk + blockIdx.x];
+    {   // boff[d] = (exclusive scan of the digit totals)[d] + this tile's prefix within d
+        __shared__ uint32_t s_ws[kRsThreads / 32];
+        const int per = (nbins + kRsThreads - 1) / kRsThreads;  // consecutive digits per thread
+        uint32_t tot = 0;
+        for (int k = 0; k < per; k++) {
+            const int d = t * per + k;
+            if (d < nbins) tot += dtot[d];
+        }
+        uint32_t inc = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
+        }
+        if (lane == 31) s_ws[warp] = inc;
+        __syncthreads();
+        uint32_t pre = inc - tot;
+        for (int w = 0; w < warp; w++) pre += s_ws[w];
+        for (int k = 0; k < per; k++) {
+            const int d = t * per + k;
+            if (d < nbins) {
+                boff[d] = pre + hscan[(size_t)d * nblk + blockIdx.x];
+                pre += dtot[d];
+                run[d] = 0;
+            }
+        }
     }
     for (int e = t; e < (kRsThreads / 32) * nbins; e += kRsThreads) wcnt[e] = 0;
     __syncthreads();
     const uint32_t lt = (1u << lane) - 1u;
-    const int base = blockIdx.x * kRsChunk;
-    for (int r = 0; r < kRsRounds; r++) {
+    const int base = blockIdx.x * kRsThreads * rounds;
+    for (int r = 0; r < rounds; r++) {
         const int i = base + r * kRsThreads + t;
         const bool valid = i < n;
         const uint32_t k = valid ? kin[i] : 0u;
@@ -187,112 +225,78 @@ __global__ void __launch_bounds__(kRsThreads) rs_downsweep(
     }
 }
 
-// Exclusive scan of a u32 array (length L) in place: block sums -> scan -> apply.
-constexpr int kScanChunk = 2048;
-
-__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
-    const int lane = threadIdx.x & 31;
+// Per-digit exclusive scan over the tiles, in place (hist is digit-major [d][tile]), one
+// CTA per digit (each thread a run of consecutive tiles); dtot[d] = the digit's total.
+__global__ void __launch_bounds__(256) rs_scan_digits(uint32_t* __restrict__ hist, int nbins, int nblk,
+                                                      uint32_t* __restrict__ dtot) {
+    __shared__ uint32_t s_ws[8];
+    const int d = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    uint32_t* row = hist + (size_t)d * nblk;
+    const int per = (nblk + 255) / 256;
+    const int b0 = t * per, b1 = min(b0 + per, nblk);
+    uint32_t sum = 0;
+    for (int b = b0; b < b1; b++) sum += row[b];
+    uint32_t inc = sum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += t;
+        const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += u;
     }
-    return v;
-}
-
-__global__ void __launch_bounds__(256) scan_sums_kernel(const uint32_t* __restrict__ a, int64_t L,
-                                                        uint32_t* __restrict__ sums) {
-    const int64_t base = (int64_t)blockIdx.x * kScanChunk;
-    uint32_t s = 0;
-    for (int k = threadIdx.x; k < kScanChunk; k += 256) {
-        const int64_t i = base + k;
-        if (i < L) s += a[i];
-    }
-    s = warp_incl_scan(s);  // lane 31 holds the warp total
-    __shared__ uint32_t ws[8];
-    if ((threadIdx.x & 31) == 31) ws[threadIdx.x >> 5] = s;
+    if (lane == 31) s_ws[warp] = inc;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t t = 0;
-        for (int w = 0; w < 8; w++) t += ws[w];
-        sums[blockIdx.x] = t;
+    uint32_t pre = inc - sum, tot = 0;
+    for (int w = 0; w < 8; w++) {
+        if (w < warp) pre += s_ws[w];
+        tot += s_ws[w];
     }
+    for (int b = b0; b < b1; b++) {
+        const uint32_t v = row[b];
+        row[b] = pre;
+        pre += v;
+    }
+    if (t == 0) dtot[d] = tot;
 }
 
-// single block: exclusive scan of the block sums (sequential over 256-wide slabs)
-__global__ void __launch_bounds__(256) scan_block_sums_kernel(uint32_t* __restrict__ sums, int nb) {
-    __shared__ uint32_t carry;
-    __shared__ uint32_t ws[8];
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (int base = 0; base < nb; base += 256) {
-        const int i = base + threadIdx.x;
-        const uint32_t v = i < nb ? sums[i] : 0u;
-        const uint32_t inc = warp_incl_scan(v);
-        if ((threadIdx.x & 31) == 31) ws[threadIdx.x >> 5] = inc;
-        __syncthreads();
-        uint32_t wpre = 0, tot = 0;
-        for (int w = 0; w < 8; w++) {
-            if (w < (int)(threadIdx.x >> 5)) wpre += ws[w];
-            tot += ws[w];
-        }
-        const uint32_t c0 = carry;
-        if (i < nb) sums[i] = c0 + wpre + inc - v;
-        __syncthreads();
-        if (threadIdx.x == 0) carry = c0 + tot;
-        __syncthreads();
-    }
-}
-
-__global__ void __launch_bounds__(256) scan_apply_kernel(uint32_t* __restrict__ a, int64_t L,
-                                                         const uint32_t* __restrict__ sums) {
-    // each thread owns 8 consecutive elements of the 2048-chunk
-    const int64_t base = (int64_t)blockIdx.x * kScanChunk + threadIdx.x * 8;
-    uint32_t v[8];
-    uint32_t s = 0;
-#pragma unroll
-    for (int k = 0; k < 8; k++) {
-        v[k] = (base + k < L) ? a[base + k] : 0u;
-        s += v[k];
-    }
-    const uint32_t inc = warp_incl_scan(s);
-    __shared__ uint32_t ws[8];
-    if ((threadIdx.x & 31) == 31) ws[threadIdx.x >> 5] = inc;
-    __syncthreads();
-    uint32_t wpre = 0;
-    for (int w = 0; w < (int)(threadIdx.x >> 5); w++) wpre += ws[w];
-    uint32_t run = sums[blockIdx.x] + wpre + inc - s;
-#pragma unroll
-    for (int k = 0; k < 8; k++) {
-        if (base + k < L) a[base + k] = run;
-        run += v[k];
-    }
-}
-
-// bucket offsets from the sorted keys: offsets[b] = first position with key >= b
+// bucket offsets from the sorted keys: offsets[b] = first position with key >= b.  The
+// thread of position d writes the buckets (key[d-1], key[d]] (empty buckets take the next
+// occupied bucket's start); long runs of empty buckets are written by the whole warp.
 __global__ void offsets_kernel(const uint32_t* __restrict__ skey, int n, uint32_t nb,
                                uint32_t* __restrict__ offsets) {
-    for (int d = blockIdx.x * blockDim.x + threadIdx.x; d <= n; d += gridDim.x * blockDim.x) {
-        const int64_t kprev = d > 0 ? (int64_t)skey[d - 1] : -1;
-        const int64_t k = d < n ? (int64_t)min(skey[d], nb) : (int64_t)nb;
-        for (int64_t b = kprev + 1; b <= k && b <= (int64_t)nb; b++) offsets[b] = (uint32_t)d;
+    const int lane = threadIdx.x & 31;
+    const int stride = gridDim.x * blockDim.x;
+    for (int d0 = blockIdx.x * blockDim.x; d0 <= n; d0 += stride) {  // warp-uniform trip count
+        const int d = d0 + (threadIdx.x & ~31) + lane;
+        int64_t lo = 0, hi = -1;  // buckets [lo, hi] take position d
+        if (d <= n) {
+            lo = (d > 0 ? (int64_t)skey[d - 1] : -1) + 1;
+            hi = d < n ? (int64_t)min(skey[d], nb) : (int64_t)nb;
+        }
+        const bool big = hi - lo >= 8;
+        if (!big)
+            for (int64_t b = lo; b <= hi; b++) offsets[b] = (uint32_t)d;
+        uint32_t m = __ballot_sync(0xffffffffu, big);
+        while (m) {
+            const int src = __ffs(m) - 1;
+            m &= m - 1;
+            const int64_t s0 = __shfl_sync(0xffffffffu, lo, src), s1 = __shfl_sync(0xffffffffu, hi, src);
+            const int dv = __shfl_sync(0xffffffffu, d, src);
+            for (int64_t b = s0 + lane; b <= s1; b += 32) offsets[b] = (uint32_t)dv;
+        }
     }
 }
 
-// a2 gather: sorted position -> bucket-local fp32 SoA + packed int16 ranges
-__global__ void __launch_bounds__(256) gather_kernel(const double* __restrict__ x,
-                                                     const double* __restrict__ y,
+// a2 gather: sorted position -> bucket-local fp32 SoA + packed int16 ranges, from the
+// records the convert kernel wrote in input order
+__global__ void __launch_bounds__(256) gather_kernel(const uint4* __restrict__ rec,
                                                      const uint32_t* __restrict__ perm,
-                                                     const uint32_t* __restrict__ offsets,
-                                                     uint32_t nb, Geom g,
-                                                     float2* __restrict__ xy,
-                                                     uint2* __restrict__ rng) {
+                                                     const uint32_t* __restrict__ offsets, uint32_t nb,
+                                                     float2* __restrict__ xy, uint2* __restrict__ rng) {
     const int nbin = (int)offsets[nb];
     constexpr int U = 4;
     const int tile = blockDim.x * U;
     for (int d0 = blockIdx.x * tile + threadIdx.x; d0 < nbin; d0 += gridDim.x * tile) {
         uint32_t q[U];
-        double xv[U], yv[U];
+        uint4 r[U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const int d = d0 + u * blockDim.x;
@@ -301,17 +305,14 @@ __global__ void __launch_bounds__(256) gather_kernel(const double* __restrict__ 
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const int d = d0 + u * blockDim.x;
-            xv[u] = d < nbin ? x[q[u]] : 0.0;
-            yv[u] = d < nbin ? y[q[u]] : 0.0;
+            r[u] = d < nbin ? rec[q[u]] : make_uint4(0u, 0u, 0u, 0u);
         }
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const int d = d0 + u * blockDim.x;
             if (d >= nbin) break;
-            const Binned b = bin_point(xv[u], yv[u], g, nb);
-            xy[d] = make_float2(b.lx, b.ly);
-            rng[d] = make_uint2(((uint32_t)b.ilo & 0xffffu) | ((uint32_t)b.ihi << 16),
-                                ((uint32_t)b.jlo & 0xffffu) | ((uint32_t)b.jhi << 16));
+            xy[d] = make_float2(__uint_as_float(r[u].x), __uint_as_float(r[u].y));
+            rng[d] = make_uint2(r[u].z, r[u].w);
         }
     }
 }
@@ -328,22 +329,21 @@ static int grow(void** p, size_t bytes) {
     return KDE_OK;
 }
 
-int scan_excl_u32(uint32_t* a, int64_t L, uint32_t* tmp, cudaStream_t s) {
-    if (L <= 0) return 0;
-    const int nblk = (int)((L + kScanChunk - 1) / kScanChunk);
-    scan_sums_kernel<<<nblk, 256, 0, s>>>(a, L, tmp);
-    scan_block_sums_kernel<<<1, 256, 0, s>>>(tmp, nblk);
-    scan_apply_kernel<<<nblk, 256, 0, s>>>(a, L, tmp);
-    return 3;
-}
-
 int bin_points(kde_ctx* c, const double* d_x, const double* d_y, int64_t n64) {
     const int n = (int)n64;
     PointBufs& pb = c->pb;
     const Geom& g = c->g;
     cudaStream_t s = c->stream;
     const uint32_t nb = (uint32_t)g.nbx * (uint32_t)g.nby;
-    const int nblk = (n + kRsChunk - 1) / kRsChunk;
+    int bits = 1;  // LSD passes over the key bits of [0, nb]
+    while ((1ull << bits) <= nb) bits++;
+    const int passes = (bits + kRsMaxBits - 1) / kRsMaxBits;
+    const int dbits = (bits + passes - 1) / passes;
+    const uint32_t dmask = (1u << dbits) - 1u;
+    const int nbins = (int)dmask + 1;
+    const int rounds = rs_rounds(nbins);
+    const int tile = kRsThreads * rounds;
+    const int nblk = (n + tile - 1) / tile;
     if (n64 > pb.cap || pb.key[0] == nullptr) {
         const int64_t cap = n64 > 1024 ? n64 : 1024;
         int rc = KDE_OK;
@@ -353,49 +353,48 @@ int bin_points(kde_ctx* c, const double* d_x, const double* d_y, int64_t n64) {
         rc |= grow((void**)&pb.val[1], sizeof(uint32_t) * cap);
         rc |= grow((void**)&pb.xy, sizeof(float2) * cap);
         rc |= grow((void**)&pb.rng, sizeof(uint2) * cap);
+        rc |= grow((void**)&pb.rec, sizeof(uint4) * cap);
         if (rc) return KDE_ENOMEM;
         pb.cap = cap;
     }
-    const int64_t hneed = (int64_t)2048 * (nblk > 0 ? nblk : 1);
+    const int64_t hneed = (int64_t)nbins * (nblk > 0 ? nblk : 1);
     if (hneed > pb.hist_cap) {
         if (grow((void**)&pb.hist, sizeof(uint32_t) * hneed)) return KDE_ENOMEM;
-        if (grow((void**)&pb.scan_tmp, sizeof(uint32_t) * (hneed / kScanChunk + 2))) return KDE_ENOMEM;
+        if (grow((void**)&pb.scan_tmp, sizeof(uint32_t) * 2048)) return KDE_ENOMEM;  // digit totals
         pb.hist_cap = hneed;
     }
     cudaMemsetAsync(c->d_stats, 0, 3 * sizeof(unsigned long long), s);
     if (n > 0) {
-        const int grid = (n + 1023) / 1024 < 148 * 8 ? (n + 1023) / 1024 : 148 * 8;
-        bin_convert_kernel<<<grid, 256, 0, s>>>(d_x, d_y, n, g, nb, pb.key[0], c->d_stats);
-        c->launches += 1;
-        // LSD passes over the key bits of [0, nb]
-        int bits = 1;
-        while ((1ull << bits) <= nb) bits++;
-        const int passes = (bits + kRsMaxBits - 1) / kRsMaxBits;
-        const int dbits = (bits + passes - 1) / passes;
-        const uint32_t dmask = (1u << dbits) - 1u;
-        const size_t up_smem = sizeof(uint32_t) * (dmask + 1);
-        const size_t dn_smem = sizeof(uint32_t) * 2 * (dmask + 1) + sizeof(uint16_t) * 8 * (dmask + 1);
+        const size_t up_smem = sizeof(uint32_t) * nbins;
+        const size_t dn_smem = sizeof(uint32_t) * 2 * nbins + sizeof(uint16_t) * 8 * nbins;
         static bool attr = false;
         if (!attr) {
             cudaFuncSetAttribute(rs_downsweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(sizeof(uint32_t) * 2 * 2048 + sizeof(uint16_t) * 8 * 2048));
             attr = true;
         }
+        bin_convert_kernel<<<nblk, kRsThreads, up_smem, s>>>(d_x, d_y, n, g, nb, pb.key[0], pb.rec,
+                                                             c->d_stats, dmask, pb.hist, nblk, rounds);
+        c->launches += 1;
         int cur = 0;
         for (int ps = 0; ps < passes; ps++) {
             const int shift = ps * dbits;
-            rs_upsweep<<<nblk, kRsThreads, up_smem, s>>>(pb.key[cur], n, shift, dmask, pb.hist, nblk);
-            c->launches += 2 + scan_excl_u32(pb.hist, (int64_t)(dmask + 1) * nblk, pb.scan_tmp, s);
+            if (ps > 0) {
+                rs_upsweep<<<nblk, kRsThreads, up_smem, s>>>(pb.key[cur], n, shift, dmask, pb.hist, nblk, rounds);
+                c->launches += 1;
+            }
+            rs_scan_digits<<<nbins, 256, 0, s>>>(pb.hist, nbins, nblk, pb.scan_tmp);
             rs_downsweep<<<nblk, kRsThreads, dn_smem, s>>>(pb.key[cur], ps == 0 ? nullptr : pb.val[cur],
                                                           pb.key[cur ^ 1], pb.val[cur ^ 1], n, shift,
-                                                          dmask, pb.hist, nblk);
+                                                          dmask, pb.hist, pb.scan_tmp, nblk, rounds);
+            c->launches += 2;
             cur ^= 1;
         }
         pb.perm = pb.val[cur];
         const int og = (n + 1 + 255) / 256 < 148 * 16 ? (n + 1 + 255) / 256 : 148 * 16;
         offsets_kernel<<<og, 256, 0, s>>>(pb.key[cur], n, nb, c->d_offsets);
         const int gg = (n + 1023) / 1024 < 148 * 8 ? (n + 1023) / 1024 : 148 * 8;
-        gather_kernel<<<gg, 256, 0, s>>>(d_x, d_y, pb.perm, c->d_offsets, nb, g, pb.xy, pb.rng);
+        gather_kernel<<<gg, 256, 0, s>>>(pb.rec, pb.perm, c->d_offsets, nb, pb.xy, pb.rng);
         c->launches += 2;
     } else {
         cudaMemsetAsync(c->d_offsets, 0, sizeof(uint32_t) * (nb + 1), s);

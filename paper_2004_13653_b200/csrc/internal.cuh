@@ -43,7 +43,8 @@ struct PointBufs {
     uint32_t *val[2] = {nullptr, nullptr};
     uint32_t *hist = nullptr;                  // radix per-(digit, block) counts
     int64_t hist_cap = 0;
-    uint32_t *scan_tmp = nullptr;
+    uint32_t *scan_tmp = nullptr;                // radix digit totals
+    uint4 *rec = nullptr;                      // per input point: lx, ly, packed ranges
     float2 *xy = nullptr;                      // sorted bucket-local coordinates
     uint2 *rng = nullptr;                      // sorted packed int16 ranges
     uint32_t *perm = nullptr;                  // sorted -> original index (alias)
