@@ -66,7 +66,7 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
 // ---------------------------------------------------------------------------------
 // a2 constants (the convert kernel below already works in sort tiles)
 constexpr int kRsThreads = 256;
-constexpr int kRsMaxBits = 11;
+constexpr int kRsMaxBits = 10;
 // A sort tile is kRsThreads x rounds keys, rounds = max(8, nbins / 64): tiles hold at least
 // 4 keys per digit, so the per-tile histograms stay <= 1/4 of the keys.
 inline int rs_rounds(int nbins) { return nbins / 64 > 8 ? nbins / 64 : 8; }
@@ -134,11 +134,11 @@ __global__ void __launch_bounds__(kRsThreads, 4) bin_convert_kernel(
 
 // ---------------------------------------------------------------------------------
 // a2: stable LSD counting sort.  Keys lie in [0, nb] (nb = dropped); passes =
-// ceil(bits/11) with digits of ceil(bits/passes) <= 11 bits (two passes up to 2^22
-// buckets).  Per pass: per-tile digit histograms (pass 0: fused into the convert
-// kernel) -> per-digit exclusive scan over the tiles + digit totals (one kernel) ->
-// stable in-tile ranking (warp match_any; per-warp digit counts; leaders only clear what
-// they set) + scatter, each tile adding the exclusive scan of the digit totals.
+// ceil(bits/10) with digits of ceil(bits/passes) <= 10 bits (two passes up to 2^20
+// buckets, three up to 2^30).  Per pass: per-tile digit histograms (pass 0: fused into
+// the convert kernel) -> per-digit exclusive scan over the tiles + digit totals (one
+// kernel) -> stable in-tile ranking into a digit-sorted shared-memory copy of the tile
+// -> coalesced write-out, each tile adding the exclusive scan of the digit totals.
 
 __global__ void __launch_bounds__(kRsThreads) rs_upsweep(const uint32_t* __restrict__ keys, int n,
                                                          int shift, uint32_t dmask,
@@ -157,71 +157,126 @@ __global__ void __launch_bounds__(kRsThreads) rs_upsweep(const uint32_t* __restr
     for (int d = threadIdx.x; d < nbins; d += kRsThreads) hist[(size_t)d * nblk + blockIdx.x] = h[d];
 }
 
+// exclusive scan of a[0..nb) in shared memory, in place (all kRsThreads threads call it)
+__device__ __forceinline__ void block_scan_smem(uint32_t* a, int nb, uint32_t* s_ws) {
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int per = (nb + kRsThreads - 1) / kRsThreads;  // consecutive entries per thread
+    uint32_t tot = 0;
+    for (int k = 0; k < per; k++) {
+        const int d = t * per + k;
+        if (d < nb) tot += a[d];
+    }
+    uint32_t inc = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+    }
+    if (lane == 31) s_ws[warp] = inc;
+    __syncthreads();
+    uint32_t pre = inc - tot;
+    for (int w = 0; w < warp; w++) pre += s_ws[w];
+    for (int k = 0; k < per; k++) {
+        const int d = t * per + k;
+        if (d < nb) {
+            const uint32_t v = a[d];
+            a[d] = pre;
+            pre += v;
+        }
+    }
+    __syncthreads();
+}
+
+// Stable scatter of one tile (kRsThreads x rounds keys).  Per round of 256 keys: warp
+// match_any ranks equal digits inside the warp, per-warp digit counts order the warps,
+// and a running count per digit orders the rounds; each key lands in shared memory at
+// (tile start of its digit) + (its rank among the tile's keys of that digit), so after
+// the last round the tile is sorted by digit in shared memory and is written out with
+// consecutive threads storing consecutive keys of each digit run (coalesced).
+template <bool STAGED>
 __global__ void __launch_bounds__(kRsThreads) rs_downsweep(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
     uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, int n, int shift, uint32_t dmask,
     const uint32_t* __restrict__ hscan, const uint32_t* __restrict__ dtot, int nblk, int rounds) {
     extern __shared__ uint32_t sm[];
+    __shared__ uint32_t s_ws[kRsThreads / 32];
     const int nbins = (int)dmask + 1;
-    uint32_t* run = sm;                                   // [nbins] running count per digit
-    uint32_t* boff = sm + nbins;                          // [nbins] block base per digit
-    uint16_t* wcnt = reinterpret_cast<uint16_t*>(sm + 2 * nbins);  // [8][nbins]
+    const int tile = kRsThreads * rounds;
+    uint32_t* run = sm;                     // [nbins] running count per digit
+    uint32_t* boff = sm + nbins;            // [nbins] global base of the tile's digit run
+    uint32_t* dstart = sm + 2 * nbins;      // [nbins] tile-local start of the digit run
+    uint32_t* skey = sm + 3 * nbins;        // [tile] (STAGED)
+    uint32_t* sval = skey + tile;           // [tile] (STAGED)
+    uint16_t* wcnt = reinterpret_cast<uint16_t*>(STAGED ? sval + tile : sm + 3 * nbins);  // [8][nbins]
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-    {   // boff[d] = (exclusive scan of the digit totals)[d] + this tile's prefix within d
-        __shared__ uint32_t s_ws[kRsThreads / 32];
-        const int per = (nbins + kRsThreads - 1) / kRsThreads;  // consecutive digits per thread
-        uint32_t tot = 0;
-        for (int k = 0; k < per; k++) {
-            const int d = t * per + k;
-            if (d < nbins) tot += dtot[d];
-        }
-        uint32_t inc = tot;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += v;
-        }
-        if (lane == 31) s_ws[warp] = inc;
-        __syncthreads();
-        uint32_t pre = inc - tot;
-        for (int w = 0; w < warp; w++) pre += s_ws[w];
-        for (int k = 0; k < per; k++) {
-            const int d = t * per + k;
-            if (d < nbins) {
-                boff[d] = pre + hscan[(size_t)d * nblk + blockIdx.x];
-                pre += dtot[d];
-                run[d] = 0;
-            }
-        }
+    const int b = blockIdx.x;
+    for (int d = t; d < nbins; d += kRsThreads) {
+        const uint32_t cur = hscan[(size_t)d * nblk + b];
+        const uint32_t nxt = b + 1 < nblk ? hscan[(size_t)d * nblk + b + 1] : dtot[d];
+        boff[d] = dtot[d];    // -> exclusive scan of the digit totals
+        dstart[d] = nxt - cur;  // the tile's count -> its exclusive scan
+        run[d] = cur;         // (stash: this tile's prefix within the digit)
     }
     for (int e = t; e < (kRsThreads / 32) * nbins; e += kRsThreads) wcnt[e] = 0;
     __syncthreads();
+    block_scan_smem(boff, nbins, s_ws);
+    if (STAGED) block_scan_smem(dstart, nbins, s_ws);
+    for (int d = t; d < nbins; d += kRsThreads) {
+        boff[d] += run[d];
+        run[d] = 0;
+    }
+    __syncthreads();
     const uint32_t lt = (1u << lane) - 1u;
-    const int base = blockIdx.x * kRsThreads * rounds;
-    for (int r = 0; r < rounds; r++) {
-        const int i = base + r * kRsThreads + t;
-        const bool valid = i < n;
-        const uint32_t k = valid ? kin[i] : 0u;
-        const uint32_t v = valid ? (vin ? vin[i] : (uint32_t)i) : 0u;
-        const uint32_t d = valid ? ((k >> shift) & dmask) : (0x10000u + lane);  // unique if invalid
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
-        const uint32_t lrank = __popc(peers & lt);
-        const bool leader = valid && lrank == 0;
-        if (leader) wcnt[warp * nbins + d] = (uint16_t)__popc(peers);
-        __syncthreads();
-        if (valid) {
-            uint32_t pos = run[d] + lrank;
-            for (int w = 0; w < warp; w++) pos += wcnt[w * nbins + d];
-            const uint32_t dst = boff[d] + pos;
-            kout[dst] = k;
-            vout[dst] = v;
+    const int base = b * tile;
+    constexpr int kBatch = 8;  // rounds whose keys are loaded before any is ranked
+    for (int r0 = 0; r0 < rounds; r0 += kBatch) {
+        uint32_t kb[kBatch], vb[kBatch];
+#pragma unroll
+        for (int q = 0; q < kBatch; q++) {
+            const int i = base + (r0 + q) * kRsThreads + t;
+            kb[q] = i < n ? kin[i] : 0u;
+            vb[q] = i < n ? (vin ? vin[i] : (uint32_t)i) : 0u;
         }
-        __syncthreads();
-        if (leader) {
-            atomicAdd(&run[d], (uint32_t)__popc(peers));
-            wcnt[warp * nbins + d] = 0;
+#pragma unroll
+        for (int q = 0; q < kBatch; q++) {
+            const int i = base + (r0 + q) * kRsThreads + t;
+            const bool valid = i < n;
+            const uint32_t k = kb[q], v = vb[q];
+            const uint32_t d = valid ? ((k >> shift) & dmask) : (0x10000u + lane);  // unique if invalid
+            const uint32_t peers = __match_any_sync(0xffffffffu, d);
+            const uint32_t lrank = __popc(peers & lt);
+            const bool leader = valid && lrank == 0;
+            if (leader) wcnt[warp * nbins + d] = (uint16_t)__popc(peers);
+            __syncthreads();
+            if (valid) {
+                uint32_t pos = run[d] + lrank;
+                for (int w = 0; w < warp; w++) pos += wcnt[w * nbins + d];
+                if (STAGED) {
+                    const uint32_t lp = dstart[d] + pos;
+                    skey[lp] = k;
+                    sval[lp] = v;
+                } else {
+                    const uint32_t dst = boff[d] + pos;
+                    kout[dst] = k;
+                    vout[dst] = v;
+                }
+            }
+            __syncthreads();
+            if (leader) {
+                atomicAdd(&run[d], (uint32_t)__popc(peers));
+                wcnt[warp * nbins + d] = 0;
+            }
+            __syncthreads();
         }
-        __syncthreads();
+    }
+    if (!STAGED) return;
+    const int cnt = min(tile, n - base);
+    for (int e = t; e < cnt; e += kRsThreads) {
+        const uint32_t k = skey[e];
+        const uint32_t d = (k >> shift) & dmask;
+        const uint32_t dst = boff[d] + (uint32_t)e - dstart[d];
+        kout[dst] = k;
+        vout[dst] = sval[e];
     }
 }
 
@@ -366,11 +421,17 @@ int bin_points(kde_ctx* c, const double* d_x, const double* d_y, int64_t n64) {
     cudaMemsetAsync(c->d_stats, 0, 3 * sizeof(unsigned long long), s);
     if (n > 0) {
         const size_t up_smem = sizeof(uint32_t) * nbins;
-        const size_t dn_smem = sizeof(uint32_t) * 2 * nbins + sizeof(uint16_t) * 8 * nbins;
+        // small digit sets scatter short runs: stage the tile digit-sorted in shared memory
+        // and write it out coalesced; large ones (>= 512 digits) scatter directly
+        const bool staged = nbins < 512;
+        const size_t dn_smem =
+            sizeof(uint32_t) * (3 * nbins + (staged ? 2 * tile : 0)) + sizeof(uint16_t) * 8 * nbins;
         static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(rs_downsweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(sizeof(uint32_t) * 2 * 2048 + sizeof(uint16_t) * 8 * 2048));
+        if (!attr) {  // largest case: 1024 digits, tile 256 x 16
+            cudaFuncSetAttribute(rs_downsweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(sizeof(uint32_t) * (3 * 256 + 2 * 2048) + sizeof(uint16_t) * 8 * 256));
+            cudaFuncSetAttribute(rs_downsweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(sizeof(uint32_t) * 3 * 1024 + sizeof(uint16_t) * 8 * 1024));
             attr = true;
         }
         bin_convert_kernel<<<nblk, kRsThreads, up_smem, s>>>(d_x, d_y, n, g, nb, pb.key[0], pb.rec,
@@ -384,9 +445,9 @@ int bin_points(kde_ctx* c, const double* d_x, const double* d_y, int64_t n64) {
                 c->launches += 1;
             }
             rs_scan_digits<<<nbins, 256, 0, s>>>(pb.hist, nbins, nblk, pb.scan_tmp);
-            rs_downsweep<<<nblk, kRsThreads, dn_smem, s>>>(pb.key[cur], ps == 0 ? nullptr : pb.val[cur],
-                                                          pb.key[cur ^ 1], pb.val[cur ^ 1], n, shift,
-                                                          dmask, pb.hist, pb.scan_tmp, nblk, rounds);
+            (staged ? rs_downsweep<true> : rs_downsweep<false>)<<<nblk, kRsThreads, dn_smem, s>>>(
+                pb.key[cur], ps == 0 ? nullptr : pb.val[cur], pb.key[cur ^ 1], pb.val[cur ^ 1], n, shift, dmask,
+                pb.hist, pb.scan_tmp, nblk, rounds);
             c->launches += 2;
             cur ^= 1;
         }
