@@ -142,8 +142,10 @@ KDE_API int kde_create(const kde_params* p, kde_ctx** out);
  * stats come back asynchronously; kde_get_stats waits).  Ordering: device
  * inputs are read after all work already queued on the legacy default stream
  * (PyTorch's default stream); binning starts after the context's previous
- * kde_eval has finished reading the bins; a host-input upload may overlap that
- * evaluation.  Non-finite points are dropped and not counted in n.
+ * kde_eval has finished reading the bins; a host-input upload runs on the
+ * context's copy stream into one of two staging buffers, overlapping the
+ * previous load's binning and evaluation (pinned host memory makes it
+ * asynchronous).  Non-finite points are dropped and not counted in n.
  * Errors: KDE_EINVAL (NULL ctx, n < 0, NULL x/y with n > 0, mixed host/device),
  *   KDE_ENOMEM, KDE_ECUDA.
  */

@@ -289,6 +289,10 @@ int kde_create(const kde_params* p, kde_ctx** out) {
     // a non-blocking stream: a host-input upload may overlap the previous evaluation; the
     // load orders itself explicitly (see kde_load_points)
     cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
+    for (int k = 0; k < 2 && e == cudaSuccess; k++)
+        e = cudaEventCreateWithFlags(&c->stage_free[k], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->stage_ready, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->loaded_ev, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->evald_ev, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->input_ev, cudaEventDisableTiming);
@@ -335,6 +339,7 @@ int kde_load_points(kde_ctx* c, const double* x, const double* y, int64_t n) {
     if (!dg.ok) return cuda_fail(cudaGetLastError(), "kde_load_points: cudaSetDevice");
     c->loaded = false;
     const double *dx = x, *dy = y;
+    int stage_used = -1;
     if (n > 0) {
         int devx = -1, devy = -1;
         const bool xd = is_device_ptr(x, &devx), yd = is_device_ptr(y, &devy);
@@ -347,23 +352,32 @@ int kde_load_points(kde_ctx* c, const double* x, const double* y, int64_t n) {
                       c->p.device);
             return KDE_EINVAL;
         }
-        if (!xd) {  // host input: copy into the context's staging buffers
-            if (c->pb.stage_cap < n) {
-                cudaFree(c->pb.x);
-                cudaFree(c->pb.y);
-                c->pb.x = c->pb.y = nullptr;
-                if (cudaMalloc(&c->pb.x, sizeof(double) * n) != cudaSuccess ||
-                    cudaMalloc(&c->pb.y, sizeof(double) * n) != cudaSuccess) {
+        if (!xd) {  // host input: upload on the copy stream into a staging buffer pair
+            const int j = c->pb.stage;
+            if (c->pb.stage_cap[j] < n) {
+                cudaFree(c->pb.sx[j]);
+                cudaFree(c->pb.sy[j]);
+                c->pb.sx[j] = c->pb.sy[j] = nullptr;
+                c->pb.stage_cap[j] = 0;
+                if (cudaMalloc(&c->pb.sx[j], sizeof(double) * n) != cudaSuccess ||
+                    cudaMalloc(&c->pb.sy[j], sizeof(double) * n) != cudaSuccess) {
                     cudaGetLastError();
                     set_error("kde_load_points: staging allocation failed");
                     return KDE_ENOMEM;
                 }
-                c->pb.stage_cap = n;
+                c->pb.stage_cap[j] = n;
             }
-            cudaMemcpyAsync(c->pb.x, x, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream);
-            cudaMemcpyAsync(c->pb.y, y, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream);
-            dx = c->pb.x;
-            dy = c->pb.y;
+            // the binning that last read buffer j must be done (a never-recorded event is
+            // complete); the upload then overlaps the previous load's binning and eval
+            cudaStreamWaitEvent(c->copy_stream, c->stage_free[j], 0);
+            cudaMemcpyAsync(c->pb.sx[j], x, sizeof(double) * n, cudaMemcpyHostToDevice, c->copy_stream);
+            cudaMemcpyAsync(c->pb.sy[j], y, sizeof(double) * n, cudaMemcpyHostToDevice, c->copy_stream);
+            cudaEventRecord(c->stage_ready, c->copy_stream);
+            cudaStreamWaitEvent(c->stream, c->stage_ready, 0);
+            dx = c->pb.sx[j];
+            dy = c->pb.sy[j];
+            stage_used = j;
+            c->pb.stage ^= 1;
         } else {
             // device inputs: read them after the work already queued on the legacy default
             // stream (where PyTorch's default stream puts their producers)
@@ -376,6 +390,7 @@ int kde_load_points(kde_ctx* c, const double* x, const double* y, int64_t n) {
     tmark(c, 0, c->stream);
     int rc = bin_points(c, dx, dy, n);
     if (rc) return rc;
+    if (stage_used >= 0) cudaEventRecord(c->stage_free[stage_used], c->stream);
     tmark(c, 1, c->stream);
     c->tev_load = c->timing;
     // the integer stats come back asynchronously (kde_get_stats waits for them); the
@@ -553,9 +568,12 @@ void kde_free(kde_ctx* c) {
     cudaGetDevice(&prev);
     cudaSetDevice(c->p.device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
     PointBufs& pb = c->pb;
-    cudaFree(pb.x);
-    cudaFree(pb.y);
+    for (int k = 0; k < 2; k++) {
+        cudaFree(pb.sx[k]);
+        cudaFree(pb.sy[k]);
+    }
     for (int k = 0; k < 2; k++) {
         cudaFree(pb.key[k]);
         cudaFree(pb.val[k]);
@@ -570,6 +588,10 @@ void kde_free(kde_ctx* c) {
     free_plan(c->plan[0]);
     free_plan(c->plan[1]);
     if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    for (int k = 0; k < 2; k++)
+        if (c->stage_free[k]) cudaEventDestroy(c->stage_free[k]);
+    if (c->stage_ready) cudaEventDestroy(c->stage_ready);
     if (c->loaded_ev) cudaEventDestroy(c->loaded_ev);
     if (c->evald_ev) cudaEventDestroy(c->evald_ev);
     if (c->input_ev) cudaEventDestroy(c->input_ev);

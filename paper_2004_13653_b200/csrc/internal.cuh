@@ -37,8 +37,10 @@ struct Geom {
 // Point-sized device buffers (capacity grows, never shrinks).
 struct PointBufs {
     int64_t cap = 0;
-    double *x = nullptr, *y = nullptr;         // staging of host inputs
-    int64_t stage_cap = 0;
+    double *sx[2] = {nullptr, nullptr};        // double-buffered staging of host inputs
+    double *sy[2] = {nullptr, nullptr};
+    int64_t stage_cap[2] = {0, 0};
+    int stage = 0;                             // staging buffer of the next host load
     uint32_t *key[2] = {nullptr, nullptr};     // radix ping-pong
     uint32_t *val[2] = {nullptr, nullptr};
     uint32_t *hist = nullptr;                  // radix per-(digit, block) counts
@@ -118,6 +120,9 @@ struct kde_ctx {
     int kern = 0;
     bool radial = false;
     cudaStream_t stream = nullptr;             // internal stream (loads)
+    cudaStream_t copy_stream = nullptr;        // host-input uploads (overlap the binning)
+    cudaEvent_t stage_free[2] = {};            // staging buffer k read by its binning
+    cudaEvent_t stage_ready = nullptr;         // the last upload has landed
     kde::PointBufs pb;
     uint32_t* d_offsets = nullptr;             // nb + 1
     unsigned long long* d_stats = nullptr;     // n_finite, n_outside, useful_pairs
