@@ -88,7 +88,7 @@ def report(rep):
 
 def traffic(rep, key):
     recs, units = _raw(rep)
-    d = recs[0]
+    d = [r for r in recs if key in r.get("Kernel Name", "")][0]  # first launch of that kernel
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     b = 0.0
     for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
