@@ -13,7 +13,7 @@
 namespace kde {
 
 constexpr int kSubMax = 48;       // direct-path sub-window edge bound (pixels): S = 8 TY <= 48
-constexpr int kSegPts = 512;      // split-K: points per splat work item (a constant, so the
+constexpr int kSegPts = 1024;     // split-K: points per splat work item (a constant, so the
                                   // plan is invariant under band sharding);
                                   // also bounds every fp32 running sum to 512 terms (R10)
 constexpr int kPartPtsDirect = 128;  // direct path: remainder piece = one warp's work item

@@ -114,40 +114,71 @@ __global__ void __launch_bounds__(kPlanThreads) plan_finish_kernel(
     const uint64_t* __restrict__ bsum, int nblk, int2* __restrict__ group, int4* __restrict__ items,
     int* __restrict__ totals, int* __restrict__ hot) {
     const uint64_t T = bsum[nblk];
-    const int TF = (int)(T >> 32), TP = (int)(T & 0xffffffffu);
+    const int TF = (int)(T >> 32);
     const int nsub = pg.nsub(), ng = pg.ngroups();
+    const int lane = threadIdx.x & 31;
     const int i0 = blockIdx.x * kPlanTile + threadIdx.x * kPlanPer;
     const uint64_t base = bsum[blockIdx.x];
     uint32_t chunks = 0;  // 32-point chunks of this thread's groups (tensor-core flop count)
 #pragma unroll
     for (int k = 0; k < kPlanPer; k++) {
         const int i = i0 + k;
-        if (i >= ng) break;
-        const uint64_t pre = base + local[i];
-        uint32_t cnt;
-        const uint64_t own = group_pair(g, pg, off, i, &cnt);
-        const int fs = (int)(pre >> 32), ps = (int)(pre & 0xffffffffu);
-        const int nf = (int)(own >> 32), np = (int)(own & 0xffffffffu);
-        const int sb = fs + ps;  // first segment (segments numbered group by group)
-        group[i] = make_int2(sb, nf + np);
-        if (nf + np > 1) hot[atomicAdd(&totals[kTotHot], 1)] = i;  // split group: segment reduce
-        for (int sg = 0; sg < nf; sg++)
-            for (int sub = 0; sub < nsub; sub++)
-                items[(fs + sg) * nsub + sub] =
-                    make_int4(i, sg * kSegPts, (sg + 1) * kSegPts, (sb + sg) * nsub + sub);
-        for (int k = 0; k < np; k++) {  // the remainder's pieces of <= part_pts points
-            const int k0 = nf * kSegPts + k * pg.part_pts, k1 = min(k0 + pg.part_pts, (int)cnt);
-            for (int sub = 0; sub < nsub; sub++)
-                items[(TF + ps + k) * nsub + sub] = make_int4(i, k0, k1, (sb + nf + k) * nsub + sub);
+        int fs = 0, ps = 0, nf = 0, np = 0;
+        uint32_t cnt = 0;
+        if (i < ng) {
+            const uint64_t pre = base + local[i];
+            const uint64_t own = group_pair(g, pg, off, i, &cnt);
+            fs = (int)(pre >> 32);
+            ps = (int)(pre & 0xffffffffu);
+            nf = (int)(own >> 32);
+            np = (int)(own & 0xffffffffu);
+            group[i] = make_int2(fs + ps, nf + np);  // first segment (numbered group by group)
+            if (nf + np > 1) hot[atomicAdd(&totals[kTotHot], 1)] = i;  // split group: segment reduce
+            chunks += (uint32_t)nf * (kSegPts / 32) + ((cnt % kSegPts) + 31) / 32;
         }
-        chunks += (uint32_t)nf * (kSegPts / 32) + ((cnt % kSegPts) + 31) / 32;
+        // items: a group with few is written by its own thread; the rest (hot groups have
+        // hundreds) by the whole warp, one group at a time
+        const int nit = (nf + np) * nsub;
+        const bool big = nit > 8;
+        const int sb = fs + ps;
+        if (!big) {
+            for (int e = 0; e < nf * nsub; e++) {
+                const int sg = e / nsub, sub = e % nsub;
+                items[(fs + sg) * nsub + sub] = make_int4(i, sg * kSegPts, (sg + 1) * kSegPts, (sb + sg) * nsub + sub);
+            }
+            for (int e = 0; e < np * nsub; e++) {
+                const int kk = e / nsub, sub = e % nsub;
+                const int k0 = nf * kSegPts + kk * pg.part_pts, k1 = min(k0 + pg.part_pts, (int)cnt);
+                items[(TF + ps + kk) * nsub + sub] = make_int4(i, k0, k1, (sb + nf + kk) * nsub + sub);
+            }
+        }
+        uint32_t m = __ballot_sync(0xffffffffu, big);
+        while (m) {
+            const int src = __ffs(m) - 1;
+            m &= m - 1;
+            const int gi = __shfl_sync(0xffffffffu, i, src);
+            const int gfs = __shfl_sync(0xffffffffu, fs, src), gps = __shfl_sync(0xffffffffu, ps, src);
+            const int gnf = __shfl_sync(0xffffffffu, nf, src), gnp = __shfl_sync(0xffffffffu, np, src);
+            const int gcnt = (int)__shfl_sync(0xffffffffu, cnt, src);
+            const int gsb = gfs + gps;
+            for (int e = lane; e < gnf * nsub; e += 32) {  // full segments
+                const int sg = e / nsub, sub = e % nsub;
+                items[(gfs + sg) * nsub + sub] =
+                    make_int4(gi, sg * kSegPts, (sg + 1) * kSegPts, (gsb + sg) * nsub + sub);
+            }
+            for (int e = lane; e < gnp * nsub; e += 32) {  // the remainder's pieces of <= part_pts
+                const int kk = e / nsub, sub = e % nsub;
+                const int k0 = gnf * kSegPts + kk * pg.part_pts, k1 = min(k0 + pg.part_pts, gcnt);
+                items[(TF + gps + kk) * nsub + sub] = make_int4(gi, k0, k1, (gsb + gnf + kk) * nsub + sub);
+            }
+        }
     }
     chunks = __reduce_add_sync(0xffffffffu, chunks);
-    if ((threadIdx.x & 31) == 0 && chunks) atomicAdd(&totals[kTotChunks], (int)chunks);
+    if (lane == 0 && chunks) atomicAdd(&totals[kTotChunks], (int)chunks);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         totals[kTotFull] = TF;
-        totals[kTotPart] = TP;
-        totals[kTotSlots] = (TF + TP) * nsub;
+        totals[kTotPart] = (int)(T & 0xffffffffu);
+        totals[kTotSlots] = (TF + (int)(T & 0xffffffffu)) * nsub;
         totals[kTotBinned] = (int)off[g.nbx * g.nby];
     }
 }
