@@ -66,7 +66,7 @@ static void plan_geometry_direct(EvalPlan& pl, const Geom& g) {
     pg.sx = pg.sy = (Wd + pg.nsubx - 1) / pg.nsubx;  // the last sub-window may be smaller
     pl.mt = std::max(2, (pg.sx + 7) / 8);            // TY
     pg.slot_w = pg.slot_h = 8 * pl.mt;               // S x S slot (float4-aligned rows)
-    pg.part_pts = kPartPtsDirect;                    // remainders: one warp per 128 points
+    pl.part_fixed = true;                            // remainders: one warp per 128 points
     pl.enabled = true;
 }
 
@@ -114,6 +114,8 @@ static int alloc_plan(EvalPlan& pl) {
 // trip -- unless the splat bound exceeds the context's budget (very large windows): then
 // the exact slot count is read back once and only that much is allocated.
 static int plan_path(kde_ctx* c, EvalPlan& pl, cudaStream_t s) {
+    pl.pg.seg_pts = seg_pts_for(c->stats.n_in);  // global n: identical on every rank
+    pl.pg.part_pts = pl.part_fixed ? std::min(kPartPtsDirect, pl.pg.seg_pts) : pl.pg.seg_pts;
     const int64_t bound = slot_bound(pl.pg, c->stats.n_in);
     if (bound + 1 > pl.items_cap) {
         if (dalloc((void**)&pl.d_items, sizeof(int4) * (bound + 1), "plan items")) return KDE_ENOMEM;

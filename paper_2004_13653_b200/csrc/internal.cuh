@@ -13,9 +13,17 @@
 namespace kde {
 
 constexpr int kSubMax = 48;       // direct-path sub-window edge bound (pixels): S = 8 TY <= 48
-constexpr int kSegPts = 1024;     // split-K: points per splat work item (a constant, so the
-                                  // plan is invariant under band sharding);
-                                  // also bounds every fp32 running sum to 512 terms (R10)
+// split-K: points per full splat work item ("segment"), chosen per load from the global
+// point count (seg_pts_for below) -- the same on every rank, so the plan is invariant under
+// band sharding; <= 4096 keeps every per-warp fp32 running sum of the direct
+// path within 512 terms (R10)
+constexpr int kSegMin = 512, kSegMax = 4096;
+constexpr int64_t kSegShareCtas = 1184;  // 148 SMs x 8 tensor-core CTAs
+inline int seg_pts_for(int64_t n) {
+    int seg = kSegMin;
+    while (seg < kSegMax && 3 * (int64_t)(2 * seg) <= 2 * (n / kSegShareCtas)) seg *= 2;
+    return seg;
+}
 constexpr int kPartPtsDirect = 128;  // direct path: remainder piece = one warp's work item
 constexpr int kCombTile = 32;     // combine-pass output tile edge
 constexpr int kTcM = 128;         // tensor-core tile rows = TMEM lanes
@@ -64,8 +72,10 @@ struct PathGeom {
     int nsubx = 1, nsuby = 1;
     int sx = 0, sy = 0;
     int slot_w = 0, slot_h = 0;
-    int part_pts = kSegPts;  // a group's remainder (< kSegPts points) is cut into pieces of
-                             // <= part_pts points, one work item each (direct: 128, one warp)
+    int seg_pts = kSegMin;   // points per full segment (set per load, seg_pts_for)
+    int part_pts = 0;        // a group's remainder (< seg_pts points) is cut into pieces of <=
+                             // part_pts points, one work item each (direct: 128, one warp;
+                             // 0: the whole remainder, = seg_pts)
     __host__ __device__ int nsub() const { return nsubx * nsuby; }
     __host__ __device__ int ngroups() const { return ngx * ngy; }
     __host__ __device__ int64_t slot_floats() const { return (int64_t)slot_w * slot_h; }
@@ -77,6 +87,7 @@ struct EvalPlan {
     // SIMT splat launch shape (direct path)
     int mt = 4;                                // lane tile rows TY (columns 2 TY), S = 8 TY
     int grid = 0;                              // persistent grid (0: not yet queried)
+    bool part_fixed = false;                   // remainder pieces of kPartPtsDirect (direct)
     int64_t planned_gen = -1;                  // load generation this plan belongs to
     // device buffers.  The plan's sizes stay on the device (kTot*): kernels read them, the
     // host never waits for them (buffers are reserved at their upper bounds).
@@ -107,8 +118,8 @@ constexpr int kTotInts = 8;
 // sub-windows.
 inline int64_t slot_bound(const PathGeom& pg, int64_t n) {
     const int64_t ng = (int64_t)pg.ngroups();
-    const int64_t rem = pg.part_pts < kSegPts ? n / pg.part_pts : 0;
-    return (n / kSegPts + rem + (n < ng ? n : ng)) * pg.nsub();
+    const int64_t rem = pg.part_pts < pg.seg_pts ? n / pg.part_pts : 0;
+    return (n / pg.seg_pts + rem + (n < ng ? n : ng)) * pg.nsub();
 }
 
 }  // namespace kde

@@ -4,8 +4,8 @@
 // path's group is a vertical stack of pg.s buckets (1 for the direct path).
 //
 //   plan_local    per group g whose window meets the band: cnt_g = sum of its buckets'
-//                 counts, full_g = cnt_g / kSegPts full segments, part_g =
-//                 ceil((cnt_g % kSegPts) / pg.part_pts) remainder pieces;
+//                 counts, full_g = cnt_g / pg.seg_pts full segments, part_g =
+//                 ceil((cnt_g % pg.seg_pts) / pg.part_pts) remainder pieces;
 //                 block-local exclusive scan of the packed pair (full_g << 32 | part_g)
 //   plan_blocks   one CTA: exclusive scan of the block totals
 //   plan_finish   global prefixes -> group[g] = (first segment, #segments), the item list
@@ -42,8 +42,8 @@ __device__ __forceinline__ uint64_t group_pair(const Geom& g, const PathGeom& pg
     if (wy1 < g.rb || wy0 > g.re - 1) return 0;  // window misses the band
     const uint32_t c = group_count(g, pg, off, gx, gy);
     *cnt = c;
-    const uint32_t rem = c % kSegPts;
-    return ((uint64_t)(c / kSegPts) << 32) | (uint64_t)((rem + pg.part_pts - 1) / pg.part_pts);
+    const uint32_t rem = c % pg.seg_pts;
+    return ((uint64_t)(c / pg.seg_pts) << 32) | (uint64_t)((rem + pg.part_pts - 1) / pg.part_pts);
 }
 
 // block-wide exclusive scan of one u64 per thread (kPlanThreads threads); returns the total
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_finish_kernel(
             np = (int)(own & 0xffffffffu);
             group[i] = make_int2(fs + ps, nf + np);  // first segment (numbered group by group)
             if (nf + np > 1) hot[atomicAdd(&totals[kTotHot], 1)] = i;  // split group: segment reduce
-            chunks += (uint32_t)nf * (kSegPts / 32) + ((cnt % kSegPts) + 31) / 32;
+            chunks += (uint32_t)nf * (pg.seg_pts / 32) + ((cnt % pg.seg_pts) + 31) / 32;
         }
         // items: a group with few is written by its own thread; the rest (hot groups have
         // hundreds) by the whole warp, one group at a time
@@ -144,11 +144,11 @@ __global__ void __launch_bounds__(kPlanThreads) plan_finish_kernel(
         if (!big) {
             for (int e = 0; e < nf * nsub; e++) {
                 const int sg = e / nsub, sub = e % nsub;
-                items[(fs + sg) * nsub + sub] = make_int4(i, sg * kSegPts, (sg + 1) * kSegPts, (sb + sg) * nsub + sub);
+                items[(fs + sg) * nsub + sub] = make_int4(i, sg * pg.seg_pts, (sg + 1) * pg.seg_pts, (sb + sg) * nsub + sub);
             }
             for (int e = 0; e < np * nsub; e++) {
                 const int kk = e / nsub, sub = e % nsub;
-                const int k0 = nf * kSegPts + kk * pg.part_pts, k1 = min(k0 + pg.part_pts, (int)cnt);
+                const int k0 = nf * pg.seg_pts + kk * pg.part_pts, k1 = min(k0 + pg.part_pts, (int)cnt);
                 items[(TF + ps + kk) * nsub + sub] = make_int4(i, k0, k1, (sb + nf + kk) * nsub + sub);
             }
         }
@@ -164,11 +164,11 @@ __global__ void __launch_bounds__(kPlanThreads) plan_finish_kernel(
             for (int e = lane; e < gnf * nsub; e += 32) {  // full segments
                 const int sg = e / nsub, sub = e % nsub;
                 items[(gfs + sg) * nsub + sub] =
-                    make_int4(gi, sg * kSegPts, (sg + 1) * kSegPts, (gsb + sg) * nsub + sub);
+                    make_int4(gi, sg * pg.seg_pts, (sg + 1) * pg.seg_pts, (gsb + sg) * nsub + sub);
             }
             for (int e = lane; e < gnp * nsub; e += 32) {  // the remainder's pieces of <= part_pts
                 const int kk = e / nsub, sub = e % nsub;
-                const int k0 = gnf * kSegPts + kk * pg.part_pts, k1 = min(k0 + pg.part_pts, gcnt);
+                const int k0 = gnf * pg.seg_pts + kk * pg.part_pts, k1 = min(k0 + pg.part_pts, gcnt);
                 items[(TF + gps + kk) * nsub + sub] = make_int4(gi, k0, k1, (gsb + gnf + kk) * nsub + sub);
             }
         }
