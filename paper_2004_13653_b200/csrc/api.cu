@@ -90,6 +90,8 @@ static void plan_geometry_tc(EvalPlan& pl, const Geom& g, bool gaussian_product)
     pg.sy = pg.wh;
     pg.slot_w = ((Wd + 15) / 16) * 16;  // MMA N
     pg.slot_h = kTcM;
+    pg.chunk_pts = 32;                  // 2 MMAs per operand buffer (eval_tc.cu, H = 1; 64-point
+                                        // chunks measured slower: 5 CTAs/SM instead of 8)
 }
 
 static int alloc_plan(EvalPlan& pl) {
@@ -504,8 +506,8 @@ int kde_get_stats(const kde_ctx* c, kde_stats* s) {
         int chunks = 0;
         const cudaError_t e = cudaMemcpy(&chunks, tp.d_totals + kTotChunks, sizeof(int), cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) return cuda_fail(e, "kde_get_stats");
-        // per 32-point chunk: two M=128 x N x K=16 MMAs, 2 flops per MAC
-        s->tc_mma_flops = (int64_t)chunks * 2 * 2 * kTcM * tp.pg.slot_w * 16;
+        // per chunk: chunk_pts/16 MMAs of M=128 x N x K=16, 2 flops per MAC
+        s->tc_mma_flops = (int64_t)chunks * (tp.pg.chunk_pts / 16) * 2 * kTcM * tp.pg.slot_w * 16;
     }
     return KDE_OK;
 }

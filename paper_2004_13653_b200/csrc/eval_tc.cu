@@ -31,9 +31,16 @@
 namespace kde {
 
 constexpr int kTcThreads = 128;
-constexpr int kTcChunk = 32;                  // points per chunk (2 MMAs of K = 16)
-constexpr int kTcABytes = kTcM * kTcChunk * 2;  // 8 KB per A buffer
+constexpr int kIssuer = 96;  // the thread that issues the MMAs and commits
 constexpr int kMaxStack = 32;
+// H points per lane per chunk: a chunk is 32 H points = 2 H MMAs of K = 16; the A buffer
+// is 128 x 32H fp16 (8H KB); 8-row core-matrix groups are 512 H bytes apart (SBO)
+template <int H> struct TcShape {
+    static constexpr int kChunk = 32 * H;
+    static constexpr int kABytes = kTcM * kChunk * 2;
+    static constexpr int kSBO = 512 * H;
+    static constexpr int kMinBlocks = H == 1 ? 8 : 5;  // CTAs per SM (smem, TMEM, registers)
+};
 
 struct TcArgs {
     Geom g;
@@ -155,7 +162,10 @@ __device__ __forceinline__ void gauss_unit(uint32_t dst, int c0, float ph, int l
     sts128(dst, o);
 }
 
-__global__ void __launch_bounds__(kTcThreads, 8) tc_splat_kernel(const TcArgs a) {
+template <int H>
+__global__ void __launch_bounds__(kTcThreads, TcShape<H>::kMinBlocks) tc_splat_kernel(const TcArgs a) {
+    using SH = TcShape<H>;
+    constexpr int kTcChunk = SH::kChunk, kTcABytes = SH::kABytes, kSBO = SH::kSBO;
     extern __shared__ __align__(1024) char tc_smem[];
     // [A0 | A1 | B0 | B1] operand buffers, then bookkeeping
     __shared__ __align__(8) uint64_t s_bar[3];  // operand buffers 0/1 freed; accumulator ready
@@ -166,7 +176,7 @@ __global__ void __launch_bounds__(kTcThreads, 8) tc_splat_kernel(const TcArgs a)
     const Geom& g = a.g;
     const PathGeom& pg = a.pg;
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-    const int bbytes = a.n * kTcChunk * 2;
+    const int bbytes = a.n * kTcChunk * 2;  // B buffer: N x 32H fp16
     const uint32_t idesc = (1u << 4)                       // D: f32
                            | (1u << 15) | (1u << 16)        // A, B: MN-major
                            | ((uint32_t)(a.n >> 3) << 17)   // N
@@ -215,42 +225,60 @@ __global__ void __launch_bounds__(kTcThreads, 8) tc_splat_kernel(const TcArgs a)
         __syncthreads();
         const uint32_t base0 = s_pre[0];
         const int cnt = it.z - it.y;
-        const int nch = (cnt + kTcChunk - 1) / kTcChunk;
+        const int nch = (cnt + kTcChunk - 1) / kTcChunk;  // (partial chunks: zero operands)
         const float shx = (float)(gx * g.B - ox) - 0.5f;   // (c + 1/2) - P = c - (P - 1/2)
-        // lane's point position, its bucket within the stack (nondecreasing in q), prefetch
+        // the lane's points q + 32h of each chunk, their buckets within the stack (kb is
+        // nondecreasing in q), prefetched one chunk ahead
         int q = it.y + lane;
         int kb = 0;
-        float2 nl = make_float2(0.f, 0.f);
-        uint2 nr = make_uint2(0u, 0u);
-        int nk = 0;
-        if (q < it.z) {
-            while (kb + 1 < ns && base0 + (uint32_t)q >= s_pre[kb + 1]) kb++;
-            nl = a.xy[base0 + q];
-            nr = a.rng[base0 + q];
-            nk = kb;
+        float2 nl[H];
+        uint2 nr[H];
+        int nk[H];
+#pragma unroll
+        for (int h = 0; h < H; h++) {
+            const int qh = q + 32 * h;
+            nl[h] = make_float2(0.f, 0.f);
+            nr[h] = make_uint2(0u, 0u);
+            nk[h] = 0;
+            if (qh < it.z) {
+                while (kb + 1 < ns && base0 + (uint32_t)qh >= s_pre[kb + 1]) kb++;
+                nl[h] = a.xy[base0 + qh];
+                nr[h] = a.rng[base0 + qh];
+                nk[h] = kb;
+            }
         }
         for (int ch = 0; ch < nch; ch++) {
             const int b = ch & 1;
-            const float2 l = nl;
-            const uint2 rr = nr;
-            const int by = gy * pg.s + nk;
-            const bool valid = q < it.z;
-            q += kTcChunk;
-            if (q < it.z) {  // prefetch the next chunk's point
-                while (kb + 1 < ns && base0 + (uint32_t)q >= s_pre[kb + 1]) kb++;
-                nl = a.xy[base0 + q];
-                nr = a.rng[base0 + q];
-                nk = kb;
+            float pxh[H], pyh[H];
+            int ilo[H], ispan[H], jlo[H], jspan[H];
+#pragma unroll
+            for (int h = 0; h < H; h++) {
+                const float2 l = nl[h];
+                const uint2 rr = nr[h];
+                const int by = gy * pg.s + nk[h];
+                const bool valid = q + 32 * h < it.z;
+                pxh[h] = pyh[h] = 0.f;
+                ilo[h] = jlo[h] = 1 << 29;
+                ispan[h] = jspan[h] = 0;
+                if (valid) {
+                    pxh[h] = l.x + shx;
+                    pyh[h] = l.y + ((float)(by * g.B - oy) - 0.5f);
+                    ilo[h] = (int)(rr.x & 0xffffu) - ox;
+                    ispan[h] = (int)(rr.x >> 16) - (int)(rr.x & 0xffffu);
+                    jlo[h] = (int)(rr.y & 0xffffu) - oy;
+                    jspan[h] = (int)(rr.y >> 16) - (int)(rr.y & 0xffffu);
+                }
             }
-            float pxh = 0.f, pyh = 0.f;
-            int ilo = 1 << 29, ispan = 0, jlo = 1 << 29, jspan = 0;
-            if (valid) {
-                pxh = l.x + shx;
-                pyh = l.y + ((float)(by * g.B - oy) - 0.5f);
-                ilo = (int)(rr.x & 0xffffu) - ox;
-                ispan = (int)(rr.x >> 16) - (int)(rr.x & 0xffffu);
-                jlo = (int)(rr.y & 0xffffu) - oy;
-                jspan = (int)(rr.y >> 16) - (int)(rr.y & 0xffffu);
+            q += kTcChunk;
+#pragma unroll
+            for (int h = 0; h < H; h++) {  // prefetch the next chunk's points
+                const int qh = q + 32 * h;
+                if (qh < it.z) {
+                    while (kb + 1 < ns && base0 + (uint32_t)qh >= s_pre[kb + 1]) kb++;
+                    nl[h] = a.xy[base0 + qh];
+                    nr[h] = a.rng[base0 + qh];
+                    nk[h] = kb;
+                }
             }
             // the MMAs that last read this buffer must be done
             if (nuse[b] > 0) mbar_wait(&s_bar[b], (nuse[b] - 1) & 1);
@@ -259,18 +287,22 @@ __global__ void __launch_bounds__(kTcThreads, 8) tc_splat_kernel(const TcArgs a)
 #pragma unroll
             for (int j = 0; j < kTcM / 32; j++) {  // A: 16 row units, 4 per warp
                 const int u = warp + 4 * j;
-                gauss_unit(ab + u * 512, u * 8, pyh, jlo, jspan, a.kq, a.q2);
+#pragma unroll
+                for (int h = 0; h < H; h++)
+                    gauss_unit(ab + u * kSBO + h * 512, u * 8, pyh[h], jlo[h], jspan[h], a.kq, a.q2);
             }
             for (int u = warp; u < nbu; u += 4)    // B: N/8 column units
-                gauss_unit(bb + u * 512, u * 8, pxh, ilo, ispan, a.kq, a.q2);
+#pragma unroll
+                for (int h = 0; h < H; h++)
+                    gauss_unit(bb + u * kSBO + h * 512, u * 8, pxh[h], ilo[h], ispan[h], a.kq, a.q2);
             fence_async_smem();
             __syncthreads();
-            if (t == 0) {
+            if (t == kIssuer) {  // warp 3 generates the fewest B units
                 tc_fence_after();
 #pragma unroll
-                for (int kk = 0; kk < 2; kk++) {
-                    const uint64_t ad = umma_desc(sm_a + b * kTcABytes + kk * 256, 128, 512);
-                    const uint64_t bd = umma_desc(sm_b + b * bbytes + kk * 256, 128, 512);
+                for (int kk = 0; kk < 2 * H; kk++) {
+                    const uint64_t ad = umma_desc(sm_a + b * kTcABytes + kk * 256, 128, kSBO);
+                    const uint64_t bd = umma_desc(sm_b + b * bbytes + kk * 256, 128, kSBO);
                     mma_f16(tmem, ad, bd, idesc, (ch > 0 || kk > 0) ? 1u : 0u);
                 }
                 mma_commit(&s_bar[b]);
@@ -303,6 +335,31 @@ __global__ void __launch_bounds__(kTcThreads, 8) tc_splat_kernel(const TcArgs a)
     }
 }
 
+template <int H>
+static void launch_tc_h(kde_ctx* c, EvalPlan& pl, const TcArgs& a, cudaStream_t s) {
+    const size_t smem = 2 * (size_t)TcShape<H>::kABytes + 2 * (size_t)a.n * TcShape<H>::kChunk * 2 + 1024;
+    if (pl.grid <= 0) {
+        cudaFuncSetAttribute(tc_splat_kernel<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int nsm = 148, per = 0;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->p.device);
+        const cudaError_t oe =
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tc_splat_kernel<H>, kTcThreads, smem);
+        if (getenv("KDE_DEBUG"))
+            fprintf(stderr, "[kde] tc occupancy query: err=%d per=%d smem=%zu\n", (int)oe, per, smem);
+        // (the occupancy API reports 1 CTA/SM for this kernel; size from the real limits:
+        //  shared memory, registers, and TMEM columns below)
+        if (oe != cudaSuccess) cudaGetLastError();
+        per = std::max(per, std::min(TcShape<H>::kMinBlocks, (int)((200u << 10) / (smem + 2048))));
+        // persistent CTAs hold their TMEM allocation for the whole launch: never
+        // oversubscribe the 512 columns of an SM
+        per = std::max(1, std::min(per, 512 / a.tmem_cols));
+        pl.grid = nsm * per;
+    }
+    cudaMemsetAsync(pl.d_totals + kTotQueue, 0, sizeof(int), s);  // work-queue head
+    tmark(c, 3, s);
+    tc_splat_kernel<H><<<pl.grid, kTcThreads, smem, s>>>(a);  // persistent; item count on device
+}
+
 int launch_tc(kde_ctx* c, float* out, cudaStream_t s) {
     EvalPlan& pl = c->plan[KDE_PATH_TENSOR];
     TcArgs a;
@@ -320,27 +377,8 @@ int launch_tc(kde_ctx* c, float* out, cudaStream_t s) {
     while (a.tmem_cols < a.n) a.tmem_cols <<= 1;
     a.kq = (float)(-0.5 * 1.4426950408889634074 / (c->hpx * c->hpx));
     a.q2 = (float)exp2(2.0 * (double)a.kq);
-    const size_t smem = 2 * (size_t)kTcABytes + 2 * (size_t)a.n * kTcChunk * 2 + 1024;
-    if (pl.grid <= 0) {
-        cudaFuncSetAttribute(tc_splat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        int nsm = 148, per = 0;
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->p.device);
-        const cudaError_t oe =
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tc_splat_kernel, kTcThreads, smem);
-        if (getenv("KDE_DEBUG"))
-            fprintf(stderr, "[kde] tc occupancy query: err=%d per=%d smem=%zu\n", (int)oe, per, smem);
-        // (the occupancy API reports 1 CTA/SM for this kernel; size from the real limits:
-        //  shared memory, and TMEM columns below)
-        if (oe != cudaSuccess) cudaGetLastError();
-        per = std::max(per, (int)((200u << 10) / (smem + 2048)));
-        // persistent CTAs hold their TMEM allocation for the whole launch: never
-        // oversubscribe the 512 columns of an SM
-        per = std::max(1, std::min(per, 512 / a.tmem_cols));
-        pl.grid = nsm * per;
-    }
-    cudaMemsetAsync(pl.d_totals + kTotQueue, 0, sizeof(int), s);  // work-queue head
-    tmark(c, 3, s);
-    tc_splat_kernel<<<pl.grid, kTcThreads, smem, s>>>(a);  // persistent; item count on device
+    if (pl.pg.chunk_pts == 32) launch_tc_h<1>(c, pl, a, s);
+    else launch_tc_h<2>(c, pl, a, s);
     c->launches += 1;
     tmark(c, 4, s);
     launch_combine(c, pl, out, s);

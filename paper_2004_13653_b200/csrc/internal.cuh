@@ -73,6 +73,7 @@ struct PathGeom {
     int sx = 0, sy = 0;
     int slot_w = 0, slot_h = 0;
     int seg_pts = kSegMin;   // points per full segment (set per load, seg_pts_for)
+    int chunk_pts = 32;      // tensor-core path: points per MMA chunk (K of one commit group)
     int part_pts = 0;        // a group's remainder (< seg_pts points) is cut into pieces of <=
                              // part_pts points, one work item each (direct: 128, one warp;
                              // 0: the whole remainder, = seg_pts)
@@ -108,7 +109,7 @@ constexpr int kTotPart = 1;    // partial segments
 constexpr int kTotSlots = 2;   // slots = work items = (full + partial) * nsub
 constexpr int kTotBinned = 3;  // points binned
 constexpr int kTotHot = 4;     // split groups (segment reduce list length)
-constexpr int kTotChunks = 5;  // tensor-core path: 32-point MMA chunks (executed-flop count)
+constexpr int kTotChunks = 5;  // tensor-core path: chunk_pts-point MMA chunks (executed flops)
 constexpr int kTotQueue = 6;   // persistent-kernel work-queue head (CTA items)
 constexpr int kTotQueue2 = 7;  // second queue head (direct path: per-warp items)
 constexpr int kTotInts = 8;

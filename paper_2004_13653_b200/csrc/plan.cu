@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_finish_kernel(
     const int lane = threadIdx.x & 31;
     const int i0 = blockIdx.x * kPlanTile + threadIdx.x * kPlanPer;
     const uint64_t base = bsum[blockIdx.x];
-    uint32_t chunks = 0;  // 32-point chunks of this thread's groups (tensor-core flop count)
+    uint32_t chunks = 0;  // MMA chunks of this thread's groups (tensor-core flop count)
 #pragma unroll
     for (int k = 0; k < kPlanPer; k++) {
         const int i = i0 + k;
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_finish_kernel(
             np = (int)(own & 0xffffffffu);
             group[i] = make_int2(fs + ps, nf + np);  // first segment (numbered group by group)
             if (nf + np > 1) hot[atomicAdd(&totals[kTotHot], 1)] = i;  // split group: segment reduce
-            chunks += (uint32_t)nf * (pg.seg_pts / 32) + ((cnt % pg.seg_pts) + 31) / 32;
+            chunks += (uint32_t)nf * (pg.seg_pts / pg.chunk_pts) + ((cnt % pg.seg_pts) + pg.chunk_pts - 1) / pg.chunk_pts;
         }
         // items: a group with few is written by its own thread; the rest (hot groups have
         // hundreds) by the whole warp, one group at a time
