@@ -72,6 +72,17 @@ struct WLayout {
     __device__ static int rowoff(int my) { return COLS + my * TYP + (my >= 4 ? SKEW : 0); }
 };
 
+// acc.{x,y} += a.{x,y} * b as one packed FFMA2 (fma.rn.f32x2: same FMA rate as FFMA,
+// half the issue slots; each half is an ordinary RN fp32 fma)
+__device__ __forceinline__ void ffma2(float2& acc, float2 a, float b) {
+    unsigned long long c = *reinterpret_cast<unsigned long long*>(&acc);
+    const float2 bb = make_float2(b, b);
+    asm("fma.rn.f32x2 %0, %1, %2, %0;"
+        : "+l"(c)
+        : "l"(*reinterpret_cast<const unsigned long long*>(&a)), "l"(*reinterpret_cast<const unsigned long long*>(&bb)));
+    acc = *reinterpret_cast<float2*>(&c);
+}
+
 // N consecutive floats from a 16-byte aligned shared address, widest loads first
 template <int N>
 __device__ __forceinline__ void lds_n(const float* p, float* v) {
@@ -158,7 +169,7 @@ __device__ __forceinline__ ItemGeo item_geo(const SplatArgs& a, const int4& it, 
 // this warp's factor buffer wbuf (warp-synchronous; no CTA barrier).  The next chunk's
 // point is loaded while the current one is evaluated.
 template <int KERN, bool RADIAL, int TY, bool RECUR>
-__device__ __forceinline__ void run_chunks(float (&acc)[TY][2 * TY], const SplatArgs& a, const ItemGeo& ig,
+__device__ __forceinline__ void run_chunks(float2 (&acc)[TY][TY], const SplatArgs& a, const ItemGeo& ig,
                                            float* wbuf, int ch0, int step, int lane) {
     using L = WLayout<TY>;
     constexpr int TX = L::TX;
@@ -205,12 +216,13 @@ __device__ __forceinline__ void run_chunks(float (&acc)[TY][2 * TY], const Splat
 #pragma unroll
             for (int r = 0; r < TY; r++)
 #pragma unroll
-                for (int c = 0; c < TX; c++) {
+                for (int c = 0; c < TX; c += 2) {
                     if constexpr (RADIAL) {
-                        const float r2 = vx[c] + vy[r];
-                        acc[r][c] += (r2 <= a.c2) ? khat_r<KERN>(r2) : 0.f;
+                        const float r0 = vx[c] + vy[r], r1 = vx[c + 1] + vy[r];
+                        acc[r][c / 2].x += (r0 <= a.c2) ? khat_r<KERN>(r0) : 0.f;
+                        acc[r][c / 2].y += (r1 <= a.c2) ? khat_r<KERN>(r1) : 0.f;
                     } else {
-                        acc[r][c] = fmaf(vy[r], vx[c], acc[r][c]);
+                        ffma2(acc[r][c / 2], make_float2(vx[c], vx[c + 1]), vy[r]);
                     }
                 }
         }
@@ -243,11 +255,11 @@ __global__ void __launch_bounds__(kWarps * 32, 2) splat_kernel(const SplatArgs a
         if (w >= ncoop) break;
         const int4 it = a.items[w];
         const ItemGeo ig = item_geo(a, it, yaxis);
-        float acc[TY][TX];
+        float2 acc[TY][TY];  // column pairs
 #pragma unroll
         for (int r = 0; r < TY; r++)
 #pragma unroll
-            for (int c = 0; c < TX; c++) acc[r][c] = 0.f;
+            for (int c = 0; c < TY; c++) acc[r][c] = make_float2(0.f, 0.f);
         run_chunks<KERN, RADIAL, TY, RECUR>(acc, a, ig, wbuf, warp, kWarps, lane);
         __syncthreads();  // every warp is done with its factor buffer
         {
@@ -255,8 +267,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) splat_kernel(const SplatArgs a
 #pragma unroll
             for (int r = 0; r < TY; r++)
 #pragma unroll
-                for (int c = 0; c < TX; c += 2)
-                    *reinterpret_cast<float2*>(red + r * S + c) = make_float2(acc[r][c], acc[r][c + 1]);
+                for (int c = 0; c < TX; c += 2) *reinterpret_cast<float2*>(red + r * S + c) = acc[r][c / 2];
         }
         __syncthreads();
         float* sp = a.splat + (size_t)it.w * slot_floats;
@@ -278,18 +289,17 @@ __global__ void __launch_bounds__(kWarps * 32, 2) splat_kernel(const SplatArgs a
         if (w >= nitems) break;
         const int4 it = a.items[w];
         const ItemGeo ig = item_geo(a, it, yaxis);
-        float acc[TY][TX];
+        float2 acc[TY][TY];
 #pragma unroll
         for (int r = 0; r < TY; r++)
 #pragma unroll
-            for (int c = 0; c < TX; c++) acc[r][c] = 0.f;
+            for (int c = 0; c < TY; c++) acc[r][c] = make_float2(0.f, 0.f);
         run_chunks<KERN, RADIAL, TY, RECUR>(acc, a, ig, wbuf, 0, 1, lane);
         float* sp = a.splat + (size_t)it.w * slot_floats + (my * TY) * S + mx * TX;
 #pragma unroll
         for (int r = 0; r < TY; r++)
 #pragma unroll
-            for (int c = 0; c < TX; c += 2)
-                *reinterpret_cast<float2*>(sp + r * S + c) = make_float2(acc[r][c], acc[r][c + 1]);
+            for (int c = 0; c < TX; c += 2) *reinterpret_cast<float2*>(sp + r * S + c) = acc[r][c / 2];
     }
 }
 
