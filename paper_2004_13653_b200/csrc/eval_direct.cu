@@ -157,7 +157,7 @@ __device__ __forceinline__ ItemGeo item_geo(const SplatArgs& a, const int4& it, 
     const int ox = gx * g.B - g.F + (sub % a.pg.nsubx) * SX;  // global pixel origin of the
     const int oy = gy * g.B - g.F + (sub / a.pg.nsubx) * SX;  // sub-window
     ItemGeo r;
-    r.base = a.offsets[gx * g.nby + gy] + (uint32_t)it.y;
+    r.base = (uint32_t)it.y;  // items hold absolute sorted positions
     r.cnt = it.z - it.y;
     r.oo = yaxis ? oy : ox;
     // exact small-integer shift, minus 1/2

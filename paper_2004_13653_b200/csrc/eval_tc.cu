@@ -218,12 +218,11 @@ __global__ void __launch_bounds__(kTcThreads, TcShape<H>::kMinBlocks) tc_splat_k
         const int gx = it.x % pg.ngx, gy = it.x / pg.ngx;
         const int ox = gx * pg.px - g.F, oy = gy * pg.py - g.F;  // window origin (pixels)
         // the stack's buckets are the contiguous keys gx*nby + gy*s + k (column-major keys):
-        // s_pre[k] = first position of bucket k relative to the stack's first point
+        // s_pre[k] = first sorted position of bucket k of the stack (items are absolute)
         const int key0 = gx * g.nby + gy * pg.s;
         const int ns = min(pg.s, g.nby - gy * pg.s);
         if (t <= ns) s_pre[t] = a.offsets[key0 + t];
         __syncthreads();
-        const uint32_t base0 = s_pre[0];
         const int cnt = it.z - it.y;
         const int nch = (cnt + kTcChunk - 1) / kTcChunk;  // (partial chunks: zero operands)
         const float shx = (float)(gx * g.B - ox) - 0.5f;   // (c + 1/2) - P = c - (P - 1/2)
@@ -241,9 +240,9 @@ __global__ void __launch_bounds__(kTcThreads, TcShape<H>::kMinBlocks) tc_splat_k
             nr[h] = make_uint2(0u, 0u);
             nk[h] = 0;
             if (qh < it.z) {
-                while (kb + 1 < ns && base0 + (uint32_t)qh >= s_pre[kb + 1]) kb++;
-                nl[h] = a.xy[base0 + qh];
-                nr[h] = a.rng[base0 + qh];
+                while (kb + 1 < ns && (uint32_t)qh >= s_pre[kb + 1]) kb++;
+                nl[h] = a.xy[qh];
+                nr[h] = a.rng[qh];
                 nk[h] = kb;
             }
         }
@@ -274,9 +273,9 @@ __global__ void __launch_bounds__(kTcThreads, TcShape<H>::kMinBlocks) tc_splat_k
             for (int h = 0; h < H; h++) {  // prefetch the next chunk's points
                 const int qh = q + 32 * h;
                 if (qh < it.z) {
-                    while (kb + 1 < ns && base0 + (uint32_t)qh >= s_pre[kb + 1]) kb++;
-                    nl[h] = a.xy[base0 + qh];
-                    nr[h] = a.rng[base0 + qh];
+                    while (kb + 1 < ns && (uint32_t)qh >= s_pre[kb + 1]) kb++;
+                    nl[h] = a.xy[qh];
+                    nr[h] = a.rng[qh];
                     nk[h] = kb;
                 }
             }

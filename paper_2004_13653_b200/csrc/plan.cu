@@ -12,7 +12,7 @@
 //                 (all full segments first -- equal work -- then the remainder pieces of
 //                 <= pg.part_pts points, segment = full segment or remainder piece;
 //                 item = (g, k0, k1, slot), slot = (first segment + seg)*nsub + sub, [k0, k1)
-//                 positions in the concatenation of the group's bucket ranges) and totals
+//                 absolute sorted positions: a group is one contiguous range) and totals
 //
 // The plan depends only on each group's own counts, so a banded context plans every group
 // it shares with the unbanded one identically (bitwise sharding).
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_finish_kernel(
 #pragma unroll
     for (int k = 0; k < kPlanPer; k++) {
         const int i = i0 + k;
-        int fs = 0, ps = 0, nf = 0, np = 0;
+        int fs = 0, ps = 0, nf = 0, np = 0, gst = 0;
         uint32_t cnt = 0;
         if (i < ng) {
             const uint64_t pre = base + local[i];
@@ -133,6 +133,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_finish_kernel(
             nf = (int)(own >> 32);
             np = (int)(own & 0xffffffffu);
             group[i] = make_int2(fs + ps, nf + np);  // first segment (numbered group by group)
+            gst = (int)off[(i % pg.ngx) * g.nby + (i / pg.ngx) * pg.s];  // group's first position
             if (nf + np > 1) hot[atomicAdd(&totals[kTotHot], 1)] = i;  // split group: segment reduce
             chunks += (uint32_t)nf * (pg.seg_pts / pg.chunk_pts) + ((cnt % pg.seg_pts) + pg.chunk_pts - 1) / pg.chunk_pts;
         }
@@ -144,12 +145,13 @@ __global__ void __launch_bounds__(kPlanThreads) plan_finish_kernel(
         if (!big) {
             for (int e = 0; e < nf * nsub; e++) {
                 const int sg = e / nsub, sub = e % nsub;
-                items[(fs + sg) * nsub + sub] = make_int4(i, sg * pg.seg_pts, (sg + 1) * pg.seg_pts, (sb + sg) * nsub + sub);
+                items[(fs + sg) * nsub + sub] =
+                    make_int4(i, gst + sg * pg.seg_pts, gst + (sg + 1) * pg.seg_pts, (sb + sg) * nsub + sub);
             }
             for (int e = 0; e < np * nsub; e++) {
                 const int kk = e / nsub, sub = e % nsub;
                 const int k0 = nf * pg.seg_pts + kk * pg.part_pts, k1 = min(k0 + pg.part_pts, (int)cnt);
-                items[(TF + ps + kk) * nsub + sub] = make_int4(i, k0, k1, (sb + nf + kk) * nsub + sub);
+                items[(TF + ps + kk) * nsub + sub] = make_int4(i, gst + k0, gst + k1, (sb + nf + kk) * nsub + sub);
             }
         }
         uint32_t m = __ballot_sync(0xffffffffu, big);
@@ -160,16 +162,17 @@ __global__ void __launch_bounds__(kPlanThreads) plan_finish_kernel(
             const int gfs = __shfl_sync(0xffffffffu, fs, src), gps = __shfl_sync(0xffffffffu, ps, src);
             const int gnf = __shfl_sync(0xffffffffu, nf, src), gnp = __shfl_sync(0xffffffffu, np, src);
             const int gcnt = (int)__shfl_sync(0xffffffffu, cnt, src);
+            const int ggst = __shfl_sync(0xffffffffu, gst, src);
             const int gsb = gfs + gps;
             for (int e = lane; e < gnf * nsub; e += 32) {  // full segments
                 const int sg = e / nsub, sub = e % nsub;
                 items[(gfs + sg) * nsub + sub] =
-                    make_int4(gi, sg * pg.seg_pts, (sg + 1) * pg.seg_pts, (gsb + sg) * nsub + sub);
+                    make_int4(gi, ggst + sg * pg.seg_pts, ggst + (sg + 1) * pg.seg_pts, (gsb + sg) * nsub + sub);
             }
             for (int e = lane; e < gnp * nsub; e += 32) {  // the remainder's pieces of <= part_pts
                 const int kk = e / nsub, sub = e % nsub;
                 const int k0 = gnf * pg.seg_pts + kk * pg.part_pts, k1 = min(k0 + pg.part_pts, gcnt);
-                items[(TF + gps + kk) * nsub + sub] = make_int4(gi, k0, k1, (gsb + gnf + kk) * nsub + sub);
+                items[(TF + gps + kk) * nsub + sub] = make_int4(gi, ggst + k0, ggst + k1, (gsb + gnf + kk) * nsub + sub);
             }
         }
     }
