@@ -145,7 +145,10 @@ KDE_API int kde_create(const kde_params* p, kde_ctx** out);
  * kde_eval has finished reading the bins; a host-input upload runs on the
  * context's copy stream into one of two staging buffers, overlapping the
  * previous load's binning and evaluation (pinned host memory makes it
- * asynchronous).  Non-finite points are dropped and not counted in n.
+ * asynchronous: the caller keeps pinned x, y unchanged until the load has
+ * completed -- e.g. until a later kde_eval's stream reaches that eval, or
+ * kde_get_stats returns; pageable memory is copied before the call returns).
+ * Non-finite points are dropped and not counted in n.
  * Errors: KDE_EINVAL (NULL ctx, n < 0, NULL x/y with n > 0, mixed host/device),
  *   KDE_ENOMEM, KDE_ECUDA.
  */
