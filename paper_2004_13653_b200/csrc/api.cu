@@ -88,7 +88,8 @@ static void plan_geometry_tc(EvalPlan& pl, const Geom& g, bool gaussian_product)
     pg.nsubx = pg.nsuby = 1;
     pg.sx = pg.ww;
     pg.sy = pg.wh;
-    pg.slot_w = ((Wd + 15) / 16) * 16;  // MMA N
+    pg.slot_w = ((Wd + 3) / 4) * 4;     // the window's columns (float4 rows); MMA N = round16
+    pg.mma_n = ((Wd + 15) / 16) * 16;
     pg.slot_h = kTcM;
     pg.chunk_pts = 32;                  // 2 MMAs per operand buffer (eval_tc.cu, H = 1; 64-point
                                         // chunks measured slower: 5 CTAs/SM instead of 8)
@@ -507,7 +508,7 @@ int kde_get_stats(const kde_ctx* c, kde_stats* s) {
         const cudaError_t e = cudaMemcpy(&chunks, tp.d_totals + kTotChunks, sizeof(int), cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) return cuda_fail(e, "kde_get_stats");
         // per chunk: chunk_pts/16 MMAs of M=128 x N x K=16, 2 flops per MAC
-        s->tc_mma_flops = (int64_t)chunks * (tp.pg.chunk_pts / 16) * 2 * kTcM * tp.pg.slot_w * 16;
+        s->tc_mma_flops = (int64_t)chunks * (tp.pg.chunk_pts / 16) * 2 * kTcM * tp.pg.mma_n * 16;
     }
     return KDE_OK;
 }

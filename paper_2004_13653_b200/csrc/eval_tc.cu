@@ -316,12 +316,13 @@ __global__ void __launch_bounds__(kTcThreads, TcShape<H>::kMinBlocks) tc_splat_k
         {
             const int row = warp * 32 + lane;
             float* dst = a.splat + (size_t)it.w * slot_floats + (size_t)row * pg.slot_w;
-            for (int c0 = 0; c0 < a.n; c0 += 16) {
+            for (int c0 = 0; c0 < a.n; c0 += 16) {  // only the window's slot_w columns
                 float v[16];
                 tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
 #pragma unroll
                 for (int k = 0; k < 16; k += 4)
-                    *reinterpret_cast<float4*>(dst + c0 + k) = make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]);
+                    if (c0 + k < pg.slot_w)
+                        *reinterpret_cast<float4*>(dst + c0 + k) = make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]);
             }
         }
         tc_fence_before();
@@ -371,7 +372,7 @@ int launch_tc(kde_ctx* c, float* out, cudaStream_t s) {
     a.group = pl.d_group;
     a.totals = pl.d_totals;
     a.splat = pl.d_splat;
-    a.n = pl.pg.slot_w;
+    a.n = pl.pg.mma_n;
     a.tmem_cols = 32;
     while (a.tmem_cols < a.n) a.tmem_cols <<= 1;
     a.kq = (float)(-0.5 * 1.4426950408889634074 / (c->hpx * c->hpx));
