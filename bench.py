@@ -39,12 +39,15 @@ CONFIGS = {
     "C2": dict(preset="estuary", n=2_000_000, W=2048, hpx=4.0, kernel="gaussian", cutoff=4.0, idx=1),
     "C3": dict(preset="promontory", n=5_000_000, W=4096, hpx=8.0, kernel="gaussian", cutoff=4.0, idx=2),
     "C4": dict(preset="islands", n=20_000_000, W=8192, hpx=4.0, kernel="gaussian", cutoff=4.0, idx=3),
+    # bandwidth sweep h = 1..32 px (--hpx); 16384^2 = 1 GiB fp32 raster
+    "C5": dict(preset="islands", n=50_000_000, W=16384, hpx=8.0, kernel="gaussian", cutoff=4.0, idx=4),
 }
 WORKLOAD = {
     "C2": "South-Channel-Yangtze-Estuary-shaped 2M points, 2048x2048, Gaussian h=4px cutoff 4h",
     "C1": "10k estuary points, 256x256, Gaussian h=2px cutoff 4h",
     "C3": "Chengshan-Jiao-Promontory-shaped 5M points, 4096x4096, h=8px",
     "C4": "Zhoushan-Islands-shaped 20M points, 8192x8192, Gaussian h=4px",
+    "C5": "Zhoushan-Islands-shaped 50M points, 16384x16384, Gaussian, bandwidth sweep h=1-32px",
 }
 METRIC = "kernel evals/sec (useful pixel-point pairs) and heatmap pixels/sec"
 UNIT = "evals/s"
@@ -147,7 +150,7 @@ def run_ours(args):
             dist.init_process_group("nccl", device_id=dev)
         else:  # validation of the N > 1 code path with several ranks on one GPU
             dist.init_process_group(args.dist_backend)
-    cfg = CONFIGS[args.config]
+    cfg = args.cfg
     W = H = cfg["W"]
     cloud, x0, y0, res = _gen(cfg)
     from paper_2004_13653_b200.dist import assemble, plan_bands
@@ -155,7 +158,7 @@ def run_ours(args):
     rows = bands[rank] if ws > 1 else (0, H)
     nrows = max(re - rb for rb, re in bands) if ws > 1 else H
     k = KDE(x0, y0, res, W, H, cfg["hpx"] * res, kernel=cfg["kernel"], cutoff=cfg["cutoff"],
-            rows=rows if ws > 1 else None, device=local)
+            radial=cfg["radial"], rows=rows if ws > 1 else None, device=local)
     xd = torch.from_numpy(cloud.x).to(dev)
     yd = torch.from_numpy(cloud.y).to(dev)
     out = torch.zeros((nrows, W), dtype=torch.float32, device=dev)
@@ -286,7 +289,7 @@ def run_ours(args):
         # (kde_stats.tc_mma_flops: 2 x 128 x N x 16 x 2 per 32-point chunk) per kernel time,
         # against the fp16 dense peak; the useful-pair share of those flops next to it
         peak = peaks["bf16_tflops"]  # fp16 dense = bf16 dense rate (guide's nominal ratio 1)
-        mma = st["tc_mma_flops"]
+        mma = st["tc_mma_flops"] * (3 if path == "tensor_split" else 1)  # split: 3 MMAs / K step
         roof = {"bound": "tensor", "kernel": "tc_splat_kernel",
                 "achieved": mma / (eval_ms * 1e-3) / 1e12,
                 "peak": peak, "unit": "TFLOP/s",
@@ -303,11 +306,13 @@ def run_ours(args):
         "metric": METRIC, "value": useful / (ms * 1e-3), "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
         "higher_is_better": True, "scaling": "strong" if ws > 1 else "weak",
-        "vs_baseline": None, "dtype": "f32" if path == "direct" else "f16xf16->f32",
+        "vs_baseline": None, "dtype": {"direct": "f32", "tensor": "f16xf16->f32",
+                                        "tensor_split": "(f16+f16)x(f16+f16)->f32"}[path],
         "data": "synthetic (aisgen, seeded)",
         "config": {"workload": WORKLOAD[args.config], "config": args.config, "path": path,
                    "n_points": cfg["n"], "grid": f"{W}x{H}", "h_px": cfg["hpx"],
                    "cutoff": cfg["cutoff"], "kernel": cfg["kernel"],
+                   "form": "radial" if cfg["radial"] else "product",
                    "parallelism": f"row-bands x{ws}" if ws > 1 else "single",
                    "l2": "flushed (512 MiB write) before every timed step"},
         "pixels_per_s": W * H / (ms * 1e-3),
@@ -329,32 +334,44 @@ def run_ours(args):
 
 
 def cpu_baseline(cfg, cloud, x0, y0, res, seconds=15.0):
-    """The oracle as it stands, timed on the host cores on a bounded sample: whole raster
-    rows (random, seeded), so the useful pairs in the sample are exact."""
+    """The oracle as it stands, timed on the host cores on a bounded sample: random (seeded)
+    row pieces of L pixels (whole rows while W*n is small; L ~ 2e10/n at C4/C5 so a piece
+    stays ~1 s of fp64 double loop), so the useful pairs in the sample are exact."""
     import oracle
     W = cfg["W"]
-    g = oracle.Grid(x0, y0, res, W, W, cfg["hpx"] * res, oracle.KERNELS.index(cfg["kernel"]),
-                    cfg["cutoff"])
+    kid = oracle.KERNELS.index(cfg["kernel"]) | (0x100 if cfg.get("radial") else 0)
+    g = oracle.Grid(x0, y0, res, W, W, cfg["hpx"] * res, kid, cfg["cutoff"])
     cores = os.cpu_count() or 1
+    n = len(cloud.x)
+    L = int(min(W, max(64, 2e10 // max(n, 1))))
     b = oracle.bin_points(g, 32, cloud.x, cloud.y)
     rng_ = b["ranges"].astype(np.int64)
-    width = rng_[:, 1] - rng_[:, 0] + 1
     rs = np.random.default_rng(7)
-    order = rs.permutation(W)
-    done_rows, pairs, t_used = 0, 0, 0.0
-    while t_used < seconds and done_rows < W:
-        take = order[done_rows:done_rows + max(1, cores)]
-        pj = np.repeat(take, W).astype(np.int32)
-        pi = np.tile(np.arange(W), len(take)).astype(np.int32)
+    npiece = W * ((W + L - 1) // L)
+    order = rs.permutation(npiece)
+    done, pairs, t_used = 0, 0, 0.0
+    while t_used < seconds and done < npiece:
+        take = order[done:done + max(1, cores)]
+        pis, pjs = [], []
+        for q in take:
+            j, i0 = int(q % W), int(q // W) * L
+            pis.append(np.arange(i0, min(i0 + L, W)))
+            pjs.append(np.full(len(pis[-1]), j))
+        pi = np.concatenate(pis).astype(np.int32)
+        pj = np.concatenate(pjs).astype(np.int32)
         t0 = time.perf_counter()
         oracle.kde_pixels(g, cloud.x, cloud.y, pi, pj, threads=cores)
         t_used += time.perf_counter() - t0
-        for j in take:
-            pairs += int(width[(rng_[:, 2] <= j) & (rng_[:, 3] >= j)].sum())
-        done_rows += len(take)
+        for q in take:
+            j, i0 = int(q % W), int(q // W) * L
+            i1 = min(i0 + L, W) - 1
+            sel = (rng_[:, 2] <= j) & (rng_[:, 3] >= j)
+            pairs += int(np.clip(np.minimum(rng_[sel, 1], i1) - np.maximum(rng_[sel, 0], i0) + 1,
+                                 0, None).sum())
+        done += len(take)
     return {"value": pairs / t_used, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{done_rows} random full rows of {W} px over all {cfg['n']} points "
-                      f"({t_used:.1f} s, fp64 double loop)",
+            "sample": f"{done} random row pieces of {L} px (of a {W}x{W} raster) over all "
+                      f"{n} points ({t_used:.1f} s, fp64 double loop)",
             "seconds": round(t_used, 2)}
 
 
@@ -362,7 +379,7 @@ def run_reference(args):
     ws, rank, _ = _dist()
     if rank != 0:
         return  # rank 0 alone runs the CPU oracle
-    cfg = CONFIGS[args.config]
+    cfg = args.cfg
     cloud, x0, y0, res = _gen(cfg)
     per = max(2.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
     import oracle
@@ -380,7 +397,8 @@ def run_reference(args):
         "data": "synthetic (aisgen, seeded)",
         "config": {"workload": WORKLOAD[args.config], "config": args.config,
                    "n_points": cfg["n"], "grid": f"{W}x{W}", "h_px": cfg["hpx"],
-                   "cutoff": cfg["cutoff"], "kernel": cfg["kernel"], "parallelism": "host threads"},
+                   "cutoff": cfg["cutoff"], "kernel": cfg["kernel"],
+                   "form": "radial" if cfg["radial"] else "product", "parallelism": "host threads"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": vals[0]["cores"], "kind": "oracle",
                          "sample": vals[0]["sample"]},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -395,12 +413,22 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2", choices=list(CONFIGS))
-    ap.add_argument("--path", default="auto", choices=["auto", "direct", "tensor"])
+    ap.add_argument("--path", default="auto", choices=["auto", "direct", "tensor", "tensor_split"])
+    ap.add_argument("--kernel", default=None, help="Table-1 kernel name (default: the config's)")
+    ap.add_argument("--radial", action="store_true", help="radial form K(||.||/h) (DESIGN.md R1)")
+    ap.add_argument("--hpx", type=float, default=None, help="bandwidth in pixels (C5 sweep)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    cfg = dict(CONFIGS[args.config])
+    if args.kernel is not None:
+        cfg["kernel"] = args.kernel
+    if args.hpx is not None:
+        cfg["hpx"] = args.hpx
+    cfg["radial"] = bool(args.radial)
+    args.cfg = cfg
     if args.impl == "reference":
         run_reference(args)
     else:

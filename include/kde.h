@@ -65,8 +65,13 @@ enum {
 /* Evaluation paths (kde_eval). */
 enum {
     KDE_PATH_DIRECT = 0, /* fp32 FMA/MUFU tiled evaluation, all kernels, both forms   */
-    KDE_PATH_TENSOR = 1  /* tcgen05 tensor-core A*B^T, product form only (fp16 operands,
+    KDE_PATH_TENSOR = 1, /* tcgen05 tensor-core A*B^T, product form of all 8 kernels
+                            (Table 1 rows are k(s)k(t); fp16 operands,
                             10-bit mantissa like tf32, fp32 accumulation in TMEM)      */
+    KDE_PATH_TENSOR_SPLIT = 2 /* the same contraction with split-fp16 operands
+                            f = hi + lo (both fp16): A_hi B_hi + A_hi B_lo + A_lo B_hi,
+                            3 MMAs per K step (3 x tc_mma_flops), ~fp32 accuracy: the
+                            DIRECT path's 1e-5 bar (NEXT-F4 accuracy mode)           */
 };
 
 /* Return codes. */
@@ -168,7 +173,7 @@ KDE_API int kde_load_points(kde_ctx* c, const double* x, const double* y, int64_
  * Deterministic: the same inputs give bitwise-identical output, and a banded
  * context gives exactly the rows of the unbanded raster.
  * Errors: KDE_EINVAL (NULL ctx/out, unknown path), KDE_ESTATE (no kde_load_points
- *   yet), KDE_EUNSUPPORTED (TENSOR with a radial kernel), KDE_ECUDA (launch error,
+ *   yet), KDE_EUNSUPPORTED (TENSOR or TENSOR_SPLIT with a radial kernel), KDE_ECUDA (launch error,
  *   or an earlier asynchronous fault).
  */
 KDE_API int kde_eval(kde_ctx* c, int32_t path, float* out, void* stream);

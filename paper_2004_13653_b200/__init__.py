@@ -14,7 +14,7 @@ from __future__ import annotations
 
 from . import _lib
 from ._lib import (KDE_COSINE, KDE_EPANECHNIKOV, KDE_GAUSSIAN, KDE_PATH_DIRECT,
-                   KDE_PATH_TENSOR, KDE_QUARTIC, KDE_RADIAL, KDE_TRIANGULAR, KDE_TRICUBE,
+                   KDE_PATH_TENSOR, KDE_PATH_TENSOR_SPLIT, KDE_QUARTIC, KDE_RADIAL, KDE_TRIANGULAR, KDE_TRICUBE,
                    KDE_TRIWEIGHT, KDE_UNIFORM, KERNEL_NAMES, KdeError, kde_create, kde_eval,
                    kde_free, kde_get_bins, kde_get_stats, kde_get_timing, kde_last_error,
                    kde_load_points, kde_params, kde_set_timing)
@@ -22,7 +22,10 @@ from ._lib import (KDE_COSINE, KDE_EPANECHNIKOV, KDE_GAUSSIAN, KDE_PATH_DIRECT,
 __all__ = ["KDE", "KdeError", "kde_params", "kde_create", "kde_load_points", "kde_eval",
            "kde_get_stats", "kde_get_bins", "kde_set_timing", "kde_get_timing", "kde_last_error",
            "kde_free", "KERNEL_NAMES",
-           "KDE_PATH_DIRECT", "KDE_PATH_TENSOR", "KDE_RADIAL", "kernel_id"]
+           "KDE_PATH_DIRECT", "KDE_PATH_TENSOR", "KDE_PATH_TENSOR_SPLIT", "KDE_RADIAL", "kernel_id"]
+
+
+_PATHS = {"direct": KDE_PATH_DIRECT, "tensor": KDE_PATH_TENSOR, "tensor_split": KDE_PATH_TENSOR_SPLIT}
 
 
 def kernel_id(name: str, radial: bool = False) -> int:
@@ -34,7 +37,7 @@ class KDE:
 
     ``KDE(x0, y0, res, W, H, h, kernel="gaussian", cutoff=4.0, radial=False,
     rows=None, device=0)``; ``load(x, y)`` bins (host or device float64 tensors);
-    ``eval(path="direct"|"tensor", out=None)`` returns the (rows, W) float32 raster.
+    ``eval(path="direct"|"tensor"|"tensor_split", out=None)`` returns the (rows, W) float32 raster.
     """
 
     def __init__(self, x0, y0, res, width, height, h, kernel="gaussian", cutoff=4.0,
@@ -54,7 +57,7 @@ class KDE:
 
     def eval(self, path="direct", out=None, stream=None):
         import torch
-        p = KDE_PATH_TENSOR if path in ("tensor", KDE_PATH_TENSOR) else KDE_PATH_DIRECT
+        p = _PATHS[path] if isinstance(path, str) else int(path)
         nr = self.rows[1] - self.rows[0]
         if out is None:
             out = torch.empty((nr, self.width), dtype=torch.float32,

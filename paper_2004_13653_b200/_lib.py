@@ -20,7 +20,7 @@ KDE_TRIWEIGHT, KDE_TRICUBE, KDE_GAUSSIAN, KDE_COSINE = 4, 5, 6, 7
 KDE_RADIAL = 0x100
 KERNEL_NAMES = ["uniform", "triangular", "epanechnikov", "quartic", "triweight", "tricube",
                 "gaussian", "cosine"]
-KDE_PATH_DIRECT, KDE_PATH_TENSOR = 0, 1
+KDE_PATH_DIRECT, KDE_PATH_TENSOR, KDE_PATH_TENSOR_SPLIT = 0, 1, 2
 KDE_OK, KDE_EINVAL, KDE_ENOMEM, KDE_ECUDA, KDE_EUNSUPPORTED, KDE_ESTATE = 0, -1, -2, -3, -4, -5
 _CODES = {KDE_EINVAL: "EINVAL", KDE_ENOMEM: "ENOMEM", KDE_ECUDA: "ECUDA",
           KDE_EUNSUPPORTED: "EUNSUPPORTED", KDE_ESTATE: "ESTATE"}

@@ -70,26 +70,30 @@ static void plan_geometry_direct(EvalPlan& pl, const Geom& g) {
     pl.enabled = true;
 }
 
-// Tensor-core geometry: a group is a vertical stack of s buckets whose window fills the
-// M = 128 TMEM lanes (rows); columns N = B + 2F rounded up to 16.  Product Gaussian only,
-// and only while B + 2F <= 128 (R_px <= ~56).
-static void plan_geometry_tc(EvalPlan& pl, const Geom& g, bool gaussian_product) {
+// Tensor-core geometry (product kernels, all eight: NEXT-F2).  While the bucket window
+// B + 2F fits the M = 128 TMEM lanes, a group is a vertical stack of s buckets whose window
+// fills them (rows); columns N = B + 2F rounded up to 16.  Larger supports (C5 at h >= 16
+// px) keep one bucket per group and cut its window into nsubx x nsuby sub-windows of
+// <= 128 rows x <= 128 columns (equal pieces), one MMA tile each (TMEM <= 128 columns:
+// 4 CTAs per SM).
+static void plan_geometry_tc(EvalPlan& pl, const Geom& g, bool product) {
     PathGeom& pg = pl.pg;
     const int Wd = g.B + 2 * g.F;
-    pl.enabled = gaussian_product && Wd <= kTcM;
+    pl.enabled = product;
     if (!pl.enabled) return;
-    pg.s = std::max(1, (kTcM - 2 * g.F) / g.B);
+    pg.s = Wd <= kTcM ? std::max(1, (kTcM - 2 * g.F) / g.B) : 1;
     pg.ngx = g.nbx;
     pg.ngy = (g.nby + pg.s - 1) / pg.s;
     pg.px = g.B;
     pg.py = pg.s * g.B;
     pg.ww = Wd;
     pg.wh = pg.py + 2 * g.F;
-    pg.nsubx = pg.nsuby = 1;
-    pg.sx = pg.ww;
-    pg.sy = pg.wh;
-    pg.slot_w = ((Wd + 3) / 4) * 4;     // the window's columns (float4 rows); MMA N = round16
-    pg.mma_n = ((Wd + 15) / 16) * 16;
+    pg.nsubx = (pg.ww + kTcM - 1) / kTcM;
+    pg.nsuby = (pg.wh + kTcM - 1) / kTcM;
+    pg.sx = (pg.ww + pg.nsubx - 1) / pg.nsubx;
+    pg.sy = (pg.wh + pg.nsuby - 1) / pg.nsuby;
+    pg.slot_w = ((pg.sx + 3) / 4) * 4;  // the sub-window's columns (float4 rows); MMA N = round16
+    pg.mma_n = ((pg.sx + 15) / 16) * 16;
     pg.slot_h = kTcM;
     pg.chunk_pts = 32;                  // 2 MMAs per operand buffer (eval_tc.cu, H = 1; 64-point
                                         // chunks measured slower: 5 CTAs/SM instead of 8)
@@ -278,7 +282,7 @@ int kde_create(const kde_params* p, kde_ctx** out) {
     }
     g.nr = (g.reach + g.B - 1) / g.B;
     plan_geometry_direct(c->plan[KDE_PATH_DIRECT], g);
-    plan_geometry_tc(c->plan[KDE_PATH_TENSOR], g, kern == KDE_GAUSSIAN && !c->radial);
+    plan_geometry_tc(c->plan[KDE_PATH_TENSOR], g, !c->radial);
     {   // kept home-bucket rows, rounded out to whole tensor-core stacks so that every group
         // of either path meeting the band is complete (bitwise sharding)
         const int st = c->plan[KDE_PATH_TENSOR].enabled ? c->plan[KDE_PATH_TENSOR].pg.s : 1;
@@ -421,7 +425,7 @@ int kde_eval(kde_ctx* c, int32_t path, float* out, void* stream) {
         set_error("kde_eval: NULL argument");
         return KDE_EINVAL;
     }
-    if (path != KDE_PATH_DIRECT && path != KDE_PATH_TENSOR) {
+    if (path != KDE_PATH_DIRECT && path != KDE_PATH_TENSOR && path != KDE_PATH_TENSOR_SPLIT) {
         set_error("kde_eval: unknown path %d", path);
         return KDE_EINVAL;
     }
@@ -429,9 +433,9 @@ int kde_eval(kde_ctx* c, int32_t path, float* out, void* stream) {
         set_error("kde_eval: no points loaded");
         return KDE_ESTATE;
     }
-    if (path == KDE_PATH_TENSOR && !c->plan[KDE_PATH_TENSOR].enabled) {
-        set_error("kde_eval: the tensor-core path implements the product-form Gaussian with "
-                  "B + 2*floor(R+1/2) <= 128 px only");
+    if (path != KDE_PATH_DIRECT && !c->plan[KDE_PATH_TENSOR].enabled) {
+        set_error("kde_eval: the tensor-core path implements the product kernels only "
+                  "(a radial support is not rank one)");
         return KDE_EUNSUPPORTED;
     }
     DeviceGuard dg(c->p.device);
@@ -442,13 +446,14 @@ int kde_eval(kde_ctx* c, int32_t path, float* out, void* stream) {
     e = cudaStreamWaitEvent(s, c->loaded_ev, 0);  // the bins of the last load
     if (e == cudaSuccess && c->evaluated) e = cudaStreamWaitEvent(s, c->evald_ev, 0);  // evals in order
     if (e != cudaSuccess) return cuda_fail(e, "kde_eval: wait for load");
-    EvalPlan& pl = c->plan[path];
+    EvalPlan& pl = c->plan[path == KDE_PATH_DIRECT ? KDE_PATH_DIRECT : KDE_PATH_TENSOR];  // (split: same plan)
     tmark(c, 2, s);
     if (pl.planned_gen != c->load_gen) {
         const int prc = plan_path(c, pl, s);
         if (prc) return prc;
     }
-    const int rc = path == KDE_PATH_DIRECT ? launch_direct(c, out, s) : launch_tc(c, out, s);
+    const int rc = path == KDE_PATH_DIRECT ? launch_direct(c, out, s)
+                                           : launch_tc(c, out, s, path == KDE_PATH_TENSOR_SPLIT);
     if (rc == KDE_OK) {
         cudaEventRecord(c->evald_ev, s);
         c->evaluated = true;

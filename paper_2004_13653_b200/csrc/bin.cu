@@ -187,89 +187,96 @@ __device__ __forceinline__ void block_scan_smem(uint32_t* a, int nb, uint32_t* s
     __syncthreads();
 }
 
-// Stable scatter of one tile (kRsThreads x rounds keys).  Per round of 256 keys: warp
-// match_any ranks equal digits inside the warp, per-warp digit counts order the warps,
-// and a running count per digit orders the rounds; each key lands in shared memory at
-// (tile start of its digit) + (its rank among the tile's keys of that digit), so after
-// the last round the tile is sorted by digit in shared memory and is written out with
-// consecutive threads storing consecutive keys of each digit run (coalesced).
-template <bool STAGED>
+// Stable scatter of one tile (kRsThreads x ROUNDS keys, ROUNDS = rs_rounds(nbins)).  Warp w
+// owns the contiguous sub-range [w*32*ROUNDS, (w+1)*32*ROUNDS) of the tile (loads stay
+// coalesced: 32 consecutive keys per round), so ranking needs no CTA barrier per round:
+//   1. per round, warp match_any ranks equal digits among the lanes; a warp-private digit
+//      counter (shared memory, uint16) orders the rounds -> rank of each key within its
+//      warp's keys of that digit (kept in registers);
+//   2. one barrier; per digit, an exclusive scan of the 8 warp counters (warp order =
+//      index order) and of the tile's digit counts (tile-local run starts);
+//   3. each key's tile-local position = run start + warp prefix + in-warp rank: STAGED
+//      writes the tile digit-sorted into shared memory and then out coalesced (small digit
+//      sets), otherwise keys scatter straight to their global positions.
+// The result is the stable order (index order within equal digits), as the oracle's
+// std::stable_sort-equivalent definition requires.
+template <bool STAGED, int ROUNDS>
 __global__ void __launch_bounds__(kRsThreads) rs_downsweep(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
     uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, int n, int shift, uint32_t dmask,
-    const uint32_t* __restrict__ hscan, const uint32_t* __restrict__ dtot, int nblk, int rounds) {
+    const uint32_t* __restrict__ hscan, const uint32_t* __restrict__ dtot, int nblk) {
     extern __shared__ uint32_t sm[];
     __shared__ uint32_t s_ws[kRsThreads / 32];
+    constexpr int kW = kRsThreads / 32;
     const int nbins = (int)dmask + 1;
-    const int tile = kRsThreads * rounds;
-    uint32_t* run = sm;                     // [nbins] running count per digit
-    uint32_t* boff = sm + nbins;            // [nbins] global base of the tile's digit run
-    uint32_t* dstart = sm + 2 * nbins;      // [nbins] tile-local start of the digit run
-    uint32_t* skey = sm + 3 * nbins;        // [tile] (STAGED)
+    constexpr int tile = kRsThreads * ROUNDS;
+    uint32_t* boff = sm;                    // [nbins] global base of the tile's digit run
+    uint32_t* dstart = sm + nbins;          // [nbins] tile-local start of the digit run
+    uint32_t* skey = sm + 2 * nbins;        // [tile] (STAGED)
     uint32_t* sval = skey + tile;           // [tile] (STAGED)
-    uint16_t* wcnt = reinterpret_cast<uint16_t*>(STAGED ? sval + tile : sm + 3 * nbins);  // [8][nbins]
+    uint16_t* wcnt = reinterpret_cast<uint16_t*>(STAGED ? sval + tile : sm + 2 * nbins);  // [kW][nbins]
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const int b = blockIdx.x;
-    for (int d = t; d < nbins; d += kRsThreads) {
-        const uint32_t cur = hscan[(size_t)d * nblk + b];
-        const uint32_t nxt = b + 1 < nblk ? hscan[(size_t)d * nblk + b + 1] : dtot[d];
-        boff[d] = dtot[d];    // -> exclusive scan of the digit totals
-        dstart[d] = nxt - cur;  // the tile's count -> its exclusive scan
-        run[d] = cur;         // (stash: this tile's prefix within the digit)
+    for (int e = t; e < kW * nbins; e += kRsThreads) wcnt[e] = 0;
+    // this warp's keys (index order: round-major within the warp's sub-range)
+    const int wbase = b * tile + warp * 32 * ROUNDS + lane;
+    uint32_t kb[ROUNDS], vb[ROUNDS], rk[ROUNDS];
+#pragma unroll
+    for (int r = 0; r < ROUNDS; r++) {
+        const int i = wbase + r * 32;
+        kb[r] = i < n ? kin[i] : 0u;
+        vb[r] = i < n ? (vin ? vin[i] : (uint32_t)i) : 0u;
     }
-    for (int e = t; e < (kRsThreads / 32) * nbins; e += kRsThreads) wcnt[e] = 0;
+    __syncthreads();
+    uint16_t* my = wcnt + warp * nbins;
+    const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int r = 0; r < ROUNDS; r++) {
+        const bool valid = wbase + r * 32 < n;
+        const uint32_t d = valid ? ((kb[r] >> shift) & dmask) : (0x10000u + lane);  // unique if invalid
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t pre = valid ? (uint32_t)my[d] : 0u;
+        rk[r] = pre + __popc(peers & lt);
+        __syncwarp();
+        if (valid && (peers & lt) == 0) my[d] = (uint16_t)(pre + __popc(peers));
+        __syncwarp();
+    }
+    __syncthreads();
+    // per digit: warp counters -> exclusive prefixes over warps; tile count -> dstart
+    for (int d = t; d < nbins; d += kRsThreads) {
+        uint32_t run = 0;
+#pragma unroll
+        for (int w = 0; w < kW; w++) {
+            const uint32_t c = wcnt[w * nbins + d];
+            wcnt[w * nbins + d] = (uint16_t)run;
+            run += c;
+        }
+        dstart[d] = run;
+        boff[d] = dtot[d];  // -> exclusive scan of the digit totals
+    }
     __syncthreads();
     block_scan_smem(boff, nbins, s_ws);
     if (STAGED) block_scan_smem(dstart, nbins, s_ws);
-    for (int d = t; d < nbins; d += kRsThreads) {
-        boff[d] += run[d];
-        run[d] = 0;
-    }
+    for (int d = t; d < nbins; d += kRsThreads) boff[d] += hscan[(size_t)d * nblk + b];  // + tile prefix
     __syncthreads();
-    const uint32_t lt = (1u << lane) - 1u;
-    const int base = b * tile;
-    constexpr int kBatch = 8;  // rounds whose keys are loaded before any is ranked
-    for (int r0 = 0; r0 < rounds; r0 += kBatch) {
-        uint32_t kb[kBatch], vb[kBatch];
 #pragma unroll
-        for (int q = 0; q < kBatch; q++) {
-            const int i = base + (r0 + q) * kRsThreads + t;
-            kb[q] = i < n ? kin[i] : 0u;
-            vb[q] = i < n ? (vin ? vin[i] : (uint32_t)i) : 0u;
-        }
-#pragma unroll
-        for (int q = 0; q < kBatch; q++) {
-            const int i = base + (r0 + q) * kRsThreads + t;
-            const bool valid = i < n;
-            const uint32_t k = kb[q], v = vb[q];
-            const uint32_t d = valid ? ((k >> shift) & dmask) : (0x10000u + lane);  // unique if invalid
-            const uint32_t peers = __match_any_sync(0xffffffffu, d);
-            const uint32_t lrank = __popc(peers & lt);
-            const bool leader = valid && lrank == 0;
-            if (leader) wcnt[warp * nbins + d] = (uint16_t)__popc(peers);
-            __syncthreads();
-            if (valid) {
-                uint32_t pos = run[d] + lrank;
-                for (int w = 0; w < warp; w++) pos += wcnt[w * nbins + d];
-                if (STAGED) {
-                    const uint32_t lp = dstart[d] + pos;
-                    skey[lp] = k;
-                    sval[lp] = v;
-                } else {
-                    const uint32_t dst = boff[d] + pos;
-                    kout[dst] = k;
-                    vout[dst] = v;
-                }
-            }
-            __syncthreads();
-            if (leader) {
-                atomicAdd(&run[d], (uint32_t)__popc(peers));
-                wcnt[warp * nbins + d] = 0;
-            }
-            __syncthreads();
+    for (int r = 0; r < ROUNDS; r++) {
+        if (wbase + r * 32 >= n) break;
+        const uint32_t d = (kb[r] >> shift) & dmask;
+        const uint32_t pos = (uint32_t)my[d] + rk[r];
+        if (STAGED) {
+            const uint32_t lp = dstart[d] + pos;
+            skey[lp] = kb[r];
+            sval[lp] = vb[r];
+        } else {
+            const uint32_t dst = boff[d] + pos;
+            kout[dst] = kb[r];
+            vout[dst] = vb[r];
         }
     }
     if (!STAGED) return;
+    __syncthreads();
+    const int base = b * tile;
     const int cnt = min(tile, n - base);
     for (int e = t; e < cnt; e += kRsThreads) {
         const uint32_t k = skey[e];
@@ -425,13 +432,14 @@ int bin_points(kde_ctx* c, const double* d_x, const double* d_y, int64_t n64) {
         // and write it out coalesced; large ones (>= 512 digits) scatter directly
         const bool staged = nbins < 512;
         const size_t dn_smem =
-            sizeof(uint32_t) * (3 * nbins + (staged ? 2 * tile : 0)) + sizeof(uint16_t) * 8 * nbins;
+            sizeof(uint32_t) * (2 * nbins + (staged ? 2 * tile : 0)) + sizeof(uint16_t) * 8 * nbins;
         static bool attr = false;
-        if (!attr) {  // largest case: 1024 digits, tile 256 x 16
-            cudaFuncSetAttribute(rs_downsweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(sizeof(uint32_t) * (3 * 256 + 2 * 2048) + sizeof(uint16_t) * 8 * 256));
-            cudaFuncSetAttribute(rs_downsweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(sizeof(uint32_t) * 3 * 1024 + sizeof(uint16_t) * 8 * 1024));
+        if (!attr) {  // largest cases: staged 256 digits x tile 2048; direct 1024 digits
+            const int st = (int)(sizeof(uint32_t) * (2 * 256 + 2 * 2048) + sizeof(uint16_t) * 8 * 256);
+            const int dr = (int)(sizeof(uint32_t) * 2 * 1024 + sizeof(uint16_t) * 8 * 1024);
+            cudaFuncSetAttribute(rs_downsweep<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, st);
+            cudaFuncSetAttribute(rs_downsweep<false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, dr);
+            cudaFuncSetAttribute(rs_downsweep<false, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, dr);
             attr = true;
         }
         bin_convert_kernel<<<nblk, kRsThreads, up_smem, s>>>(d_x, d_y, n, g, nb, pb.key[0], pb.rec,
@@ -445,9 +453,9 @@ int bin_points(kde_ctx* c, const double* d_x, const double* d_y, int64_t n64) {
                 c->launches += 1;
             }
             rs_scan_digits<<<nbins, 256, 0, s>>>(pb.hist, nbins, nblk, pb.scan_tmp);
-            (staged ? rs_downsweep<true> : rs_downsweep<false>)<<<nblk, kRsThreads, dn_smem, s>>>(
-                pb.key[cur], ps == 0 ? nullptr : pb.val[cur], pb.key[cur ^ 1], pb.val[cur ^ 1], n, shift, dmask,
-                pb.hist, pb.scan_tmp, nblk, rounds);
+            auto dsw = staged ? rs_downsweep<true, 8> : (rounds == 8 ? rs_downsweep<false, 8> : rs_downsweep<false, 16>);
+            dsw<<<nblk, kRsThreads, dn_smem, s>>>(pb.key[cur], ps == 0 ? nullptr : pb.val[cur], pb.key[cur ^ 1],
+                                                  pb.val[cur ^ 1], n, shift, dmask, pb.hist, pb.scan_tmp, nblk);
             c->launches += 2;
             cur ^= 1;
         }

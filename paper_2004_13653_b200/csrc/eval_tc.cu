@@ -54,7 +54,9 @@ struct TcArgs {
     float* __restrict__ splat;
     int n;          // MMA N
     int tmem_cols;  // allocated TMEM columns (power of two >= n)
-    float kq, q2;   // Gaussian: -log2(e)/(2 h^2), 2^(2 kq)
+    float kq, q2, q4;  // Gaussian: -log2(e)/(2 h^2), 2^(2 kq), q2^2
+    float twoc;     // Cosine: 2 cos(pi / (2 h))
+    KConst k;       // 1-D factor constants (kernels.cuh)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -138,31 +140,108 @@ __device__ __forceinline__ void sts128(uint32_t saddr, uint4 v) {
                  : "memory");
 }
 
-// 8 masked Gaussian factors of one point for the unit [c0, c0+8) -> fp16 x 8, stored as one
-// 16-byte vector at the point's slot of the operand core matrix (shared address dst).
-__device__ __forceinline__ void gauss_unit(uint32_t dst, int c0, float ph, int lo, int span, float kq,
-                                           float q2) {
-    const int l0 = max(lo - c0, 0), h0 = min(lo + span - c0, 7);
-    uint4 o = make_uint4(0u, 0u, 0u, 0u);
-    if (l0 <= h0) {
-        const uint32_t m = (2u << h0) - (1u << l0);
-        const float d0 = (float)c0 - ph;
-        float gv = ex2_ftz(d0 * d0 * kq);
-        float r = ex2_ftz(fmaf(2.0f, d0, 1.0f) * kq);
-        float f[8];
+// 8 masked 1-D kernel factors khat((c + 1/2 - P) / h) of one point for the unit
+// [c0, c0+8) -> fp16 x 8, stored as one 16-byte vector at the point's slot of the operand
+// core matrix (shared address dst).  Every Table-1 kernel is a product k(s) k(t),
+// so the same contraction serves all eight (NEXT-F2); only the factor generation differs:
+//   Gaussian  exact-ratio recurrence g(d+1) = g(d) r, r(d+1) = r(d) q^2 (2 SFU + 14 FMUL)
+//   Cosine    Chebyshev recurrence cos(a + (e+1)b) = 2 cos(b) cos(a + eb) - cos(a + (e-1)b)
+//             (2 SFU + 6 FFMA)
+//   others    the polynomial of kernels.cuh per element (FMA pipe)
+// Support membership is the fp64-decided integer range [lo, lo + span] (R3).
+// SPLIT (KDE_PATH_TENSOR_SPLIT, NEXT-F4): each factor f is also written as its fp16
+// residual lo = RN16(f - RN16(f)) into a second operand plane lo_off bytes further, so that
+// A_hi B_hi + A_hi B_lo + A_lo B_hi carries ~22 mantissa bits (the lo*lo term is 2^-22 of
+// the product): the fp32 path's 1e-5 bar on the tensor pipe.
+// Support mask of a unit as fp16x2 AND masks: entry l0*8 + h0 keeps elements l0..h0.
+__device__ __forceinline__ uint4 unit_mask(int l0, int h0) {
+    uint32_t w[4];
 #pragma unroll
-        for (int e = 0; e < 8; e++) {
-            f[e] = (m & (1u << e)) ? gv : 0.f;
-            gv *= r;
-            r *= q2;
-        }
-        o = make_uint4(pack_half2(f[0], f[1]), pack_half2(f[2], f[3]), pack_half2(f[4], f[5]),
-                       pack_half2(f[6], f[7]));
-    }
-    sts128(dst, o);
+    for (int q = 0; q < 4; q++)
+        w[q] = ((2 * q >= l0 && 2 * q <= h0) ? 0x0000ffffu : 0u) | ((2 * q + 1 >= l0 && 2 * q + 1 <= h0) ? 0xffff0000u : 0u);
+    return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-template <int H>
+__device__ __forceinline__ float2 fmul2(float2 x, float2 y) {  // mul.rn.f32x2: one issue slot
+    unsigned long long r;
+    asm("mul.rn.f32x2 %0, %1, %2;"
+        : "=l"(r)
+        : "l"(*reinterpret_cast<const unsigned long long*>(&x)), "l"(*reinterpret_cast<const unsigned long long*>(&y)));
+    return *reinterpret_cast<float2*>(&r);
+}
+
+__device__ __forceinline__ uint4 lds128(uint32_t saddr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(saddr));
+    return v;
+}
+
+// One unit of one operand buffer, warp-wide.  `dirty` (warp-uniform) tracks which of the
+// warp's units of this buffer hold non-zero data from an earlier chunk: a unit that no lane
+// touches and that is already zero is not stored again.
+template <int K, bool SPLIT>
+__device__ __forceinline__ void kern_unit(uint32_t dst, uint32_t lo_off, int c0, float ph, int lo, int span,
+                                          const TcArgs& a, uint32_t mtab, uint32_t& dirty, uint32_t bit) {
+    const int l0 = max(lo - c0, 0), h0 = min(lo + span - c0, 7);
+    const bool ne = l0 <= h0;
+    const bool any = __any_sync(0xffffffffu, ne);
+    if (!any && !(dirty & bit)) return;
+    dirty = any ? (dirty | bit) : (dirty & ~bit);
+    uint4 o = make_uint4(0u, 0u, 0u, 0u);
+    uint4 ol = make_uint4(0u, 0u, 0u, 0u);
+    if (ne) {
+        const float d0 = (float)c0 - ph;
+        float f[8];
+        if constexpr (K == KDE_GAUSSIAN) {
+            // g(d+1) = g(d) r(d), r(d+1) = r(d) q^2, two elements per packed multiply:
+            // (f[e+2], f[e+3]) = (f[e], f[e+1]) * (r_e r_{e+1}, r_{e+1} r_{e+2}), whose next
+            // value is this one * (q^4, q^4)
+            const float g0 = ex2_ftz(d0 * d0 * a.kq);
+            const float r0 = ex2_ftz(fmaf(2.0f, d0, 1.0f) * a.kq);
+            const float rr = r0 * r0;
+            float2 v = make_float2(g0, g0 * r0);
+            float2 w = fmul2(make_float2(rr, rr), make_float2(a.q2, a.q2 * a.q2 * a.q2));
+            const float2 q4 = make_float2(a.q4, a.q4);
+            f[0] = v.x;
+            f[1] = v.y;
+#pragma unroll
+            for (int e = 2; e < 8; e += 2) {
+                v = fmul2(v, w);
+                if (e < 6) w = fmul2(w, q4);
+                f[e] = v.x;
+                f[e + 1] = v.y;
+            }
+        } else if constexpr (K == KDE_COSINE) {
+            f[0] = __cosf(d0 * a.k.kc);
+            f[1] = __cosf((d0 + 1.0f) * a.k.kc);
+#pragma unroll
+            for (int e = 2; e < 8; e++) f[e] = fmaf(a.twoc, f[e - 1], -f[e - 2]);
+#pragma unroll
+            for (int e = 0; e < 8; e++) f[e] = fmaxf(f[e], 0.0f);  // DESIGN.md R8
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; e++) f[e] = khat<K>(d0 + (float)e, a.k);
+        }
+        const uint4 m = lds128(mtab + (uint32_t)(l0 * 8 + h0) * 16u);
+        o = make_uint4(pack_half2(f[0], f[1]) & m.x, pack_half2(f[2], f[3]) & m.y,
+                       pack_half2(f[4], f[5]) & m.z, pack_half2(f[6], f[7]) & m.w);
+        if constexpr (SPLIT) {
+            const uint32_t hw[4] = {o.x, o.y, o.z, o.w};
+            const uint32_t mw[4] = {m.x, m.y, m.z, m.w};
+            uint32_t lw[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const float2 hv = __half22float2(*reinterpret_cast<const __half2*>(&hw[q]));
+                lw[q] = pack_half2(f[2 * q] - hv.x, f[2 * q + 1] - hv.y) & mw[q];
+            }
+            ol = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+        }
+    }
+    sts128(dst, o);
+    if constexpr (SPLIT) sts128(dst + lo_off, ol);
+}
+
+template <int H, int K, bool SPLIT>
 __global__ void __launch_bounds__(kTcThreads, TcShape<H>::kMinBlocks) tc_splat_kernel(const TcArgs a) {
     using SH = TcShape<H>;
     constexpr int kTcChunk = SH::kChunk, kTcABytes = SH::kABytes, kSBO = SH::kSBO;
@@ -172,6 +251,7 @@ __global__ void __launch_bounds__(kTcThreads, TcShape<H>::kMinBlocks) tc_splat_k
     __shared__ uint32_t s_tmem;
     __shared__ int s_w;
     __shared__ uint32_t s_pre[kMaxStack + 1];   // first sorted position of each stack bucket
+    __shared__ uint4 s_mtab[64];                // unit support masks (unit_mask)
 
     const Geom& g = a.g;
     const PathGeom& pg = a.pg;
@@ -189,6 +269,7 @@ __global__ void __launch_bounds__(kTcThreads, TcShape<H>::kMinBlocks) tc_splat_k
                      "r"(a.tmem_cols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
+    if (t < 64) s_mtab[t] = unit_mask(t >> 3, t & 7);
     if (t == 0) {
         mbar_init(&s_bar[0], 1);
         mbar_init(&s_bar[1], 1);
@@ -200,10 +281,15 @@ __global__ void __launch_bounds__(kTcThreads, TcShape<H>::kMinBlocks) tc_splat_k
     tc_fence_after();
     const uint32_t tmem = s_tmem;
     uint32_t nuse[2] = {0u, 0u};  // commits issued per operand buffer (same on all threads)
+    uint64_t dirty = ~0ull;       // per buffer (32 bits each): this warp's units holding non-zero data
     uint32_t nacc = 0;            // accumulator-ready commits
 
-    const uint32_t sm_a = smem_u32(tc_smem);                 // A buffer b at sm_a + b * kTcABytes
-    const uint32_t sm_b = sm_a + 2 * kTcABytes;             // B buffer b at sm_b + b * bbytes
+    // A buffer b at sm_a + b * astride (SPLIT: its lo plane kTcABytes further), B buffer b
+    // at sm_b + b * bstride (lo plane bbytes further)
+    constexpr int kPlanes = SPLIT ? 2 : 1;
+    const int astride = kPlanes * kTcABytes, bstride = kPlanes * bbytes;
+    const uint32_t sm_a = smem_u32(tc_smem);
+    const uint32_t sm_b = sm_a + 2 * astride;
     const uint32_t koff = (uint32_t)((lane >> 3) * 128 + (lane & 7) * 16);  // point = k index
     const int nbu = a.n / 8;                                // B column units
     const int nitems = a.totals[kTotSlots];
@@ -216,7 +302,11 @@ __global__ void __launch_bounds__(kTcThreads, TcShape<H>::kMinBlocks) tc_splat_k
         __syncthreads();                                         // everyone has read s_w
         if (t == 0) s_w = atomicAdd(&a.totals[kTotQueue], 1);  // pop the next item early
         const int gx = it.x % pg.ngx, gy = it.x / pg.ngx;
-        const int ox = gx * pg.px - g.F, oy = gy * pg.py - g.F;  // window origin (pixels)
+        // window origin (pixels): the group's window, or its sub-window (windows wider than
+        // the 128 TMEM lanes / MMA N are cut into nsubx x nsuby pieces, slot = seg*nsub + sub)
+        const int sub = it.w % pg.nsub();
+        const int ox = gx * pg.px - g.F + (sub % pg.nsubx) * pg.sx;
+        const int oy = gy * pg.py - g.F + (sub / pg.nsubx) * pg.sy;
         // the stack's buckets are the contiguous keys gx*nby + gy*s + k (column-major keys):
         // s_pre[k] = first sorted position of bucket k of the stack (items are absolute)
         const int key0 = gx * g.nby + gy * pg.s;
@@ -281,28 +371,37 @@ __global__ void __launch_bounds__(kTcThreads, TcShape<H>::kMinBlocks) tc_splat_k
             }
             // the MMAs that last read this buffer must be done
             if (nuse[b] > 0) mbar_wait(&s_bar[b], (nuse[b] - 1) & 1);
-            const uint32_t ab = sm_a + b * kTcABytes + koff;
-            const uint32_t bb = sm_b + b * bbytes + koff;
+            const uint32_t ab = sm_a + b * astride + koff;
+            const uint32_t bb = sm_b + b * bstride + koff;
+            const uint32_t mtab = smem_u32(s_mtab);
+            uint32_t db = (uint32_t)(dirty >> (32 * b));  // bits: A units j*H + h, B units 16 + k*H + h
 #pragma unroll
             for (int j = 0; j < kTcM / 32; j++) {  // A: 16 row units, 4 per warp
                 const int u = warp + 4 * j;
 #pragma unroll
                 for (int h = 0; h < H; h++)
-                    gauss_unit(ab + u * kSBO + h * 512, u * 8, pyh[h], jlo[h], jspan[h], a.kq, a.q2);
+                    kern_unit<K, SPLIT>(ab + u * kSBO + h * 512, kTcABytes, u * 8, pyh[h], jlo[h], jspan[h], a,
+                                        mtab, db, 1u << (j * H + h));
             }
-            for (int u = warp; u < nbu; u += 4)    // B: N/8 column units
+            for (int u = warp, k = 0; u < nbu; u += 4, k++)  // B: N/8 column units
 #pragma unroll
                 for (int h = 0; h < H; h++)
-                    gauss_unit(bb + u * kSBO + h * 512, u * 8, pxh[h], ilo[h], ispan[h], a.kq, a.q2);
+                    kern_unit<K, SPLIT>(bb + u * kSBO + h * 512, bbytes, u * 8, pxh[h], ilo[h], ispan[h], a,
+                                        mtab, db, 1u << (16 + k * H + h));
+            dirty = b ? ((dirty & 0xffffffffull) | ((uint64_t)db << 32)) : ((dirty & ~0xffffffffull) | db);
             fence_async_smem();
             __syncthreads();
             if (t == kIssuer) {  // warp 3 generates the fewest B units
                 tc_fence_after();
 #pragma unroll
                 for (int kk = 0; kk < 2 * H; kk++) {
-                    const uint64_t ad = umma_desc(sm_a + b * kTcABytes + kk * 256, 128, kSBO);
-                    const uint64_t bd = umma_desc(sm_b + b * bbytes + kk * 256, 128, kSBO);
+                    const uint64_t ad = umma_desc(sm_a + b * astride + kk * 256, 128, kSBO);
+                    const uint64_t bd = umma_desc(sm_b + b * bstride + kk * 256, 128, kSBO);
                     mma_f16(tmem, ad, bd, idesc, (ch > 0 || kk > 0) ? 1u : 0u);
+                    if constexpr (SPLIT) {  // + A_hi B_lo + A_lo B_hi
+                        mma_f16(tmem, ad, umma_desc(sm_b + b * bstride + bbytes + kk * 256, 128, kSBO), idesc, 1u);
+                        mma_f16(tmem, umma_desc(sm_a + b * astride + kTcABytes + kk * 256, 128, kSBO), bd, idesc, 1u);
+                    }
                 }
                 mma_commit(&s_bar[b]);
                 if (ch == nch - 1) mma_commit(&s_bar[2]);
@@ -335,15 +434,17 @@ __global__ void __launch_bounds__(kTcThreads, TcShape<H>::kMinBlocks) tc_splat_k
     }
 }
 
-template <int H>
+template <int H, int K, bool SPLIT>
 static void launch_tc_h(kde_ctx* c, EvalPlan& pl, const TcArgs& a, cudaStream_t s) {
-    const size_t smem = 2 * (size_t)TcShape<H>::kABytes + 2 * (size_t)a.n * TcShape<H>::kChunk * 2 + 1024;
-    if (pl.grid <= 0) {
-        cudaFuncSetAttribute(tc_splat_kernel<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem =
+        (SPLIT ? 2 : 1) * (2 * (size_t)TcShape<H>::kABytes + 2 * (size_t)a.n * TcShape<H>::kChunk * 2) + 1024;
+    int& grid = SPLIT ? pl.grid_split : pl.grid;
+    if (grid <= 0) {
+        cudaFuncSetAttribute(tc_splat_kernel<H, K, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int nsm = 148, per = 0;
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->p.device);
         const cudaError_t oe =
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tc_splat_kernel<H>, kTcThreads, smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tc_splat_kernel<H, K, SPLIT>, kTcThreads, smem);
         if (getenv("KDE_DEBUG"))
             fprintf(stderr, "[kde] tc occupancy query: err=%d per=%d smem=%zu\n", (int)oe, per, smem);
         // (the occupancy API reports 1 CTA/SM for this kernel; size from the real limits:
@@ -353,14 +454,14 @@ static void launch_tc_h(kde_ctx* c, EvalPlan& pl, const TcArgs& a, cudaStream_t 
         // persistent CTAs hold their TMEM allocation for the whole launch: never
         // oversubscribe the 512 columns of an SM
         per = std::max(1, std::min(per, 512 / a.tmem_cols));
-        pl.grid = nsm * per;
+        grid = nsm * per;
     }
     cudaMemsetAsync(pl.d_totals + kTotQueue, 0, sizeof(int), s);  // work-queue head
     tmark(c, 3, s);
-    tc_splat_kernel<H><<<pl.grid, kTcThreads, smem, s>>>(a);  // persistent; item count on device
+    tc_splat_kernel<H, K, SPLIT><<<grid, kTcThreads, smem, s>>>(a);  // persistent; item count on device
 }
 
-int launch_tc(kde_ctx* c, float* out, cudaStream_t s) {
+int launch_tc(kde_ctx* c, float* out, cudaStream_t s, bool split) {
     EvalPlan& pl = c->plan[KDE_PATH_TENSOR];
     TcArgs a;
     a.g = c->g;
@@ -377,8 +478,17 @@ int launch_tc(kde_ctx* c, float* out, cudaStream_t s) {
     while (a.tmem_cols < a.n) a.tmem_cols <<= 1;
     a.kq = (float)(-0.5 * 1.4426950408889634074 / (c->hpx * c->hpx));
     a.q2 = (float)exp2(2.0 * (double)a.kq);
-    if (pl.pg.chunk_pts == 32) launch_tc_h<1>(c, pl, a, s);
-    else launch_tc_h<2>(c, pl, a, s);
+    a.q4 = (float)exp2(4.0 * (double)a.kq);
+    a.twoc = (float)(2.0 * cos(3.14159265358979323846 / (2.0 * c->hpx)));
+    a.k = make_kconst(c->hpx);
+    // chunk_pts is 32 (H = 1): 64-point chunks measured slower
+    using Fn = void (*)(kde_ctx*, EvalPlan&, const TcArgs&, cudaStream_t);
+    static const Fn kLaunch[2][8] = {
+        {launch_tc_h<1, 0, false>, launch_tc_h<1, 1, false>, launch_tc_h<1, 2, false>, launch_tc_h<1, 3, false>,
+         launch_tc_h<1, 4, false>, launch_tc_h<1, 5, false>, launch_tc_h<1, 6, false>, launch_tc_h<1, 7, false>},
+        {launch_tc_h<1, 0, true>, launch_tc_h<1, 1, true>, launch_tc_h<1, 2, true>, launch_tc_h<1, 3, true>,
+         launch_tc_h<1, 4, true>, launch_tc_h<1, 5, true>, launch_tc_h<1, 6, true>, launch_tc_h<1, 7, true>}};
+    kLaunch[split ? 1 : 0][c->kern](c, pl, a, s);
     c->launches += 1;
     tmark(c, 4, s);
     launch_combine(c, pl, out, s);

@@ -89,6 +89,7 @@ struct EvalPlan {
     // SIMT splat launch shape (direct path)
     int mt = 4;                                // lane tile rows TY (columns 2 TY), S = 8 TY
     int grid = 0;                              // persistent grid (0: not yet queried)
+    int grid_split = 0;                        // the same for the split-fp16 tensor-core kernel
     bool part_fixed = false;                   // remainder pieces of kPartPtsDirect (direct)
     int64_t planned_gen = -1;                  // load generation this plan belongs to
     // device buffers.  The plan's sizes stay on the device (kTot*): kernels read them, the
@@ -170,7 +171,7 @@ int cuda_fail(cudaError_t e, const char* what);
 int bin_points(kde_ctx* c, const double* d_x, const double* d_y, int64_t n);
 // evaluation (eval_direct.cu, eval_tc.cu)
 int launch_direct(kde_ctx* c, float* out, cudaStream_t s);
-int launch_tc(kde_ctx* c, float* out, cudaStream_t s);
+int launch_tc(kde_ctx* c, float* out, cudaStream_t s, bool split);
 // planning (plan.cu)
 int plan_device(kde_ctx* c, EvalPlan& pl, cudaStream_t s);
 int plan_nblk(const PathGeom& pg);

@@ -26,6 +26,8 @@ struct KConst {
     float kc;      // pi/(2 h_px)          (Cosine)
 };
 
+KConst make_kconst(double hpx);  // host (eval_direct.cu)
+
 // 1-D factor khat(d / h_px) (Table 1 row without its leading constant)
 template <int K>
 __device__ __forceinline__ float khat(float d, const KConst& k) {

@@ -135,7 +135,8 @@ __global__ void __launch_bounds__(kPlanThreads) plan_finish_kernel(
             group[i] = make_int2(fs + ps, nf + np);  // first segment (numbered group by group)
             gst = (int)off[(i % pg.ngx) * g.nby + (i / pg.ngx) * pg.s];  // group's first position
             if (nf + np > 1) hot[atomicAdd(&totals[kTotHot], 1)] = i;  // split group: segment reduce
-            chunks += (uint32_t)nf * (pg.seg_pts / pg.chunk_pts) + ((cnt % pg.seg_pts) + pg.chunk_pts - 1) / pg.chunk_pts;
+            chunks += ((uint32_t)nf * (pg.seg_pts / pg.chunk_pts) +
+                       ((cnt % pg.seg_pts) + pg.chunk_pts - 1) / pg.chunk_pts) * (uint32_t)nsub;
         }
         // items: a group with few is written by its own thread; the rest (hot groups have
         // hundreds) by the whole warp, one group at a time

@@ -55,6 +55,25 @@ def test_struct_layout_matches_header(tmp_path):
             assert int(out[f"{st}.{f}"]) == getattr(cls, f).offset, (st, f)
 
 
+def test_enum_values_match_header(tmp_path):
+    """The binding's constants == the header's enums (compiled with gcc)."""
+    import subprocess
+    from paper_2004_13653_b200 import _lib
+    names = ["KDE_PATH_DIRECT", "KDE_PATH_TENSOR", "KDE_PATH_TENSOR_SPLIT", "KDE_RADIAL", "KDE_OK",
+             "KDE_EINVAL", "KDE_ENOMEM", "KDE_ECUDA", "KDE_EUNSUPPORTED", "KDE_ESTATE",
+             "KDE_UNIFORM", "KDE_GAUSSIAN", "KDE_COSINE"]
+    lines = ['#include <stdio.h>', '#include "kde.h"', "int main(void){"]
+    lines += [f'printf("{n} %d\\n", (int){n});' for n in names] + ["return 0;}"]
+    src = tmp_path / "enums.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "enums"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    out = dict(l.split() for l in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                 check=True).stdout.split("\n") if l)
+    for n in names:
+        assert int(out[n]) == getattr(_lib, n), n
+
+
 def _params(**kw):
     from paper_2004_13653_b200 import _lib
     p = dict(x0=0.0, y0=0.0, res=1.0, width=64, height=64, h=2.0, kernel=6, cutoff=4.0,

@@ -243,13 +243,41 @@ def test_tensor_full_size_sampled_C2():
     assert np.abs(gpu[pj, pi] - ref).max() <= TOL_TENSOR * ref.max()
 
 
-def test_tensor_unsupported_large_support():
-    c = adversarial(hpx=20.0)  # R = 80 px: window > 128 rows
-    k = _tc(c)
-    from paper_2004_13653_b200 import KdeError
-    with pytest.raises(KdeError) as e:
-        k.eval("tensor")
-    assert e.value.code == -4
+@pytest.mark.parametrize("hpx,cutoff", [(20.0, 4.0), (36.0, 4.0), (14.0, 4.5)])
+def test_tensor_large_support_subwindows(hpx, cutoff):
+    """Windows wider than the 128 TMEM lanes (C5 at h >= 16 px): nsubx x nsuby MMA tiles."""
+    c = adversarial(W=260, H=230, n=4000, hpx=hpx)
+    k = _tc(c, cutoff=cutoff)
+    gpu = k.eval("tensor").cpu().numpy()
+    ref, _ = oracle.kde_raster(_grid(c, kernel=6, cutoff=cutoff), c["x"], c["y"], threads=THREADS)
+    assert _err(gpu, ref) <= TOL_TENSOR
+    d = k.eval("direct").cpu().numpy()
+    assert np.abs(gpu - d).max() <= TOL_TENSOR * d.max()  # O11
+
+
+# --- all eight product kernels on the tensor-core path (NEXT-F2) ----------------------------
+@pytest.mark.parametrize("kernel", range(8))
+def test_tensor_all_kernels_C1_full_raster(kernel):
+    preset, n, W, hpx, _, cut, seed = CONFIGS["C1"]
+    c = case(preset, n, W, hpx, seed=seed)
+    k = _kde(c, kernel=kernel)
+    k.load(torch.from_numpy(c["x"]).cuda(), torch.from_numpy(c["y"]).cuda())
+    gpu = k.eval("tensor").cpu().numpy()
+    ref, _ = oracle.kde_raster(_grid(c, kernel=kernel), c["x"], c["y"], threads=THREADS)
+    assert _err(gpu, ref) <= TOL_TENSOR
+
+
+@pytest.mark.parametrize("kernel", [0, 1, 5, 7])
+@pytest.mark.parametrize("hpx", [1.5, 6.0, 40.0])
+def test_tensor_all_kernels_adversarial(kernel, hpx):
+    """Ragged grid, halo points, NaN/Inf, boundary ties; compact kernels (c_eff = 1) and
+    the sub-window geometry at h = 40 px."""
+    c = adversarial(W=180 if hpx > 10 else 100, H=150 if hpx > 10 else 70, hpx=hpx)
+    k = _kde(c, kernel=kernel)
+    k.load(torch.from_numpy(c["x"]).cuda(), torch.from_numpy(c["y"]).cuda())
+    gpu = k.eval("tensor").cpu().numpy()
+    ref, _ = oracle.kde_raster(_grid(c, kernel=kernel), c["x"], c["y"], threads=THREADS)
+    assert _err(gpu, ref) <= TOL_TENSOR
 
 
 # --- C3 / C4 at full size, in the bench's configuration, on sampled pixels ------------------
@@ -290,8 +318,9 @@ def test_C3_all_kernels_direct_sampled(kernel):
     _sampled_check(_big("C3"), kernel, "direct", TOL_DIRECT)
 
 
-def test_C3_gaussian_tensor_sampled():
-    _sampled_check(_big("C3"), 6, "tensor", TOL_TENSOR)
+@pytest.mark.parametrize("kernel", range(8))
+def test_C3_all_kernels_tensor_sampled(kernel):
+    _sampled_check(_big("C3"), kernel, "tensor", TOL_TENSOR)
 
 
 @pytest.mark.parametrize("eps", [None, 0.5, 1.0, 5.0])
@@ -305,3 +334,38 @@ def test_C4_raw_and_dp_compressed(eps):
         assert 0 < keep.sum() < keep.size
     _sampled_check(c, 6, "direct", TOL_DIRECT, n_random=384)
     _sampled_check(c, 6, "tensor", TOL_TENSOR, n_random=384)
+
+
+# --- split-fp16 tensor-core accuracy mode (NEXT-F4): the DIRECT path's 1e-5 bar ---------------
+@pytest.mark.parametrize("kernel", [6, 2, 5, 7])
+def test_tensor_split_C1_full_raster(kernel):
+    preset, n, W, hpx, _, cut, seed = CONFIGS["C1"]
+    c = case(preset, n, W, hpx, seed=seed)
+    k = _kde(c, kernel=kernel)
+    k.load(torch.from_numpy(c["x"]).cuda(), torch.from_numpy(c["y"]).cuda())
+    gpu = k.eval("tensor_split").cpu().numpy()
+    ref, _ = oracle.kde_raster(_grid(c, kernel=kernel), c["x"], c["y"], threads=THREADS)
+    assert _err(gpu, ref) <= TOL_DIRECT
+
+
+@pytest.mark.parametrize("hpx", [1.5, 6.0, 36.0])
+def test_tensor_split_adversarial(hpx):
+    c = adversarial(W=260 if hpx > 10 else 100, H=230 if hpx > 10 else 70, hpx=hpx)
+    k = _tc(c)
+    gpu = k.eval("tensor_split").cpu().numpy()
+    ref, _ = oracle.kde_raster(_grid(c, kernel=6), c["x"], c["y"], threads=THREADS)
+    assert _err(gpu, ref) <= TOL_DIRECT
+    # deterministic, and the plain tensor path's plan is shared
+    np.testing.assert_array_equal(gpu.view(np.uint32), k.eval("tensor_split").cpu().numpy().view(np.uint32))
+    assert _err(k.eval("tensor").cpu().numpy(), ref) <= TOL_TENSOR
+
+
+def test_tensor_split_full_size_sampled_C2():
+    preset, n, W, hpx, _, cut, seed = CONFIGS["C2"]
+    c = case(preset, n, W, hpx, seed=seed)
+    k = _tc(c)
+    gpu = k.eval("tensor_split").cpu().numpy()
+    hx, hy = hottest_bucket_tile(c["x"], c["y"], c["x0"], c["y0"], c["res"], W, W)
+    pi, pj = sample_pixels(W, W, (0, W), gpu=gpu, tiles=[(hx, hy, 64, 64)], n_random=2048, seed=seed)
+    ref, _ = oracle.kde_pixels(_grid(c, kernel=6), c["x"], c["y"], pi, pj, threads=THREADS)
+    assert np.abs(gpu[pj, pi] - ref).max() <= TOL_DIRECT * ref.max()
