@@ -333,6 +333,87 @@ def run_ours(args):
     print(json.dumps(line), flush=True)
 
 
+def run_snap(args):
+    """--path snap: the paper's own pipeline (kde_snap: Eqs. 5-6 projection, Alg. 3 density
+    matrix with Eqs. 12-13 interpolation along the trajectories, Eq. 7 separable
+    convolution) on the config's points and grid, one GPU (other ranks exit)."""
+    import torch
+
+    from paper_2004_13653_b200 import KDE
+    ws, rank, local = _dist()
+    if rank != 0:
+        return
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    cfg = args.cfg
+    W = H = cfg["W"]
+    cloud, x0, y0, res = _gen(cfg)
+    lab = np.repeat(np.arange(len(cloud.traj_offsets) - 1, dtype=np.int32), np.diff(cloud.traj_offsets))
+    k = KDE(x0, y0, res, W, H, cfg["hpx"] * res, kernel=cfg["kernel"], cutoff=cfg["cutoff"], device=0)
+    xd, yd, ld = (torch.from_numpy(a).to(dev) for a in (cloud.x, cloud.y, lab))
+    out = torch.empty((H, W), dtype=torch.float32, device=dev)
+    cnt = torch.empty((H, W), dtype=torch.int32, device=dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        k.snap(xd, yd, ld, out=out, counts=cnt)
+    torch.cuda.synchronize()
+    launches0 = k.stats()["kernel_launches"]
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    with ClockSampler(0) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            k.snap(xd, yd, ld, out=out, counts=cnt)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    launches = k.stats()["kernel_launches"] - launches0
+    ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    # e2e: host inputs (pinned), the Eq. 7 matrix read back every step
+    xh, yh, lh = (torch.from_numpy(a).pin_memory() for a in (cloud.x, cloud.y, lab))
+    outh = torch.empty((H, W), dtype=torch.float32).pin_memory()
+    k.snap(xh, yh, lh, out=out)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        k.snap(xh, yh, lh, out=out)
+        outh.copy_(out)
+    torch.cuda.synchronize()
+    e2e = (time.perf_counter() - t0) * 1e3 / args.steps
+    a = int(np.floor((cfg["cutoff"] if cfg["kernel"] == "gaussian" else min(cfg["cutoff"], 1.0)) * cfg["hpx"]))
+    taps = W * H * (2 * a + 1) ** 2  # Eq. 7's multiply-adds (the separable form does 2(2a+1))
+    n = len(cloud.x)
+    mass = int(cnt.sum())
+    # HBM-bound: 20 B per point in (x, y, label) + per pixel M_D zero, read; tmp write, read;
+    # out write (20 B/px), plus one atomic per counted cell (interpolated cells included)
+    algo = 20 * n + 20 * W * H + 4 * mass
+    peaks, peak_src = _peaks()
+    line = {
+        "metric": "Eq. 7 kernel taps/sec of the paper's snapped pipeline (and heatmap pixels/sec)",
+        "value": taps / (ms * 1e-3), "unit": "taps/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32 counts, f32 convolution",
+        "data": "synthetic (aisgen, seeded; trajectory labels from the generator)",
+        "config": {"workload": WORKLOAD[args.config] + " - snapped pipeline (Alg. 3 + Eq. 7)",
+                   "config": args.config, "path": "snap", "n_points": n, "grid": f"{W}x{H}",
+                   "h_px": cfg["hpx"], "window_a": a, "kernel": cfg["kernel"],
+                   "interpolated_cells": mass - n, "parallelism": "single",
+                   "l2": "flushed (512 MiB write) before every timed step"},
+        "pixels_per_s": W * H / (ms * 1e-3),
+        "e2e": {"value": taps / (e2e * 1e-3), "unit": "taps/s", "ms_per_step": round(e2e, 4),
+                "h2d_bytes_per_step": 20 * n, "d2h_bytes_per_step": 4 * W * H},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "roofline": {"bound": "hbm", "kernel": "kde_snap (whole call)",
+                     "achieved": round(algo / (ms * 1e-3) / 1e9, 1), "peak": peaks["hbm_gbs"],
+                     "unit": "GB/s", "frac": round(algo / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
+                     "traffic": None, "peak_source": peak_src,
+                     "algorithmic_bytes": algo},
+    }
+    print(json.dumps(line), flush=True)
+
+
 def cpu_baseline(cfg, cloud, x0, y0, res, seconds=15.0):
     """The oracle as it stands, timed on the host cores on a bounded sample: random (seeded)
     row pieces of L pixels (whole rows while W*n is small; L ~ 2e10/n at C4/C5 so a piece
@@ -413,7 +494,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2", choices=list(CONFIGS))
-    ap.add_argument("--path", default="auto", choices=["auto", "direct", "tensor", "tensor_split"])
+    ap.add_argument("--path", default="auto", choices=["auto", "direct", "tensor", "tensor_split", "snap"])
     ap.add_argument("--kernel", default=None, help="Table-1 kernel name (default: the config's)")
     ap.add_argument("--radial", action="store_true", help="radial form K(||.||/h) (DESIGN.md R1)")
     ap.add_argument("--hpx", type=float, default=None, help="bandwidth in pixels (C5 sweep)")
@@ -431,6 +512,8 @@ def main():
     args.cfg = cfg
     if args.impl == "reference":
         run_reference(args)
+    elif args.path == "snap":
+        run_snap(args)
     else:
         run_ours(args)
 

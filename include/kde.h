@@ -213,6 +213,33 @@ typedef struct {
 KDE_API int kde_set_timing(kde_ctx* c, int enable);
 KDE_API int kde_get_timing(kde_ctx* c, kde_timing* t);
 
+/*
+ * kde_snap: the paper's own KDE pipeline, Alg. 3 + Eq. 7
+ * (PAPER.md:133-142, 167-182, 340-390), on the context's u x v = width x height matrix:
+ *   1. Eqs. 5-6: x~ = ceil((x - x_min)/(x_max - x_min) * (u - 1)) + 1 in [1, u] (y~ alike),
+ *      x_min/x_max over the finite points of this call (fp64 RN, left to right); x_max =
+ *      x_min maps every point to 1; non-finite points are skipped;
+ *   2. M_D(x~, y~) = points projected there (Alg. 3 step 2, integer atomics: exact);
+ *   3. Eqs. 12-13: adjacent points n, n+1 with label[n] == label[n+1] (Lt) and
+ *      c_max = max(|dx~|, |dy~|) > 1 add the cells [x~ + c dx~/c_max], c = 1..c_max-1,
+ *      [.] = round half up (R17-R19);
+ *   4. Eq. 7: out = f (x) M_D, f(s,t) = K(s/h_px, t/h_px) with Table 1's constants (product
+ *      form), |s|, |t| <= a = floor(c_eff h_px), zero padding; a separable two-pass fp32
+ *      convolution (exact for product kernels).
+ * Row r of M_D / out is y~ = r + 1 (row 0 = y_min), column i is x~ = i + 1.  x0, y0, res
+ * only convert h to pixels (h_px = h/res).
+ *   x, y    [in]  n fp64 coordinates, host or device (both the same kind).
+ *   label   [in]  n int32 trajectory labels (same kind as x), or NULL: no interpolation.
+ *   n       [in]  0 <= n < 2^31; n = 0 gives zeros.
+ *   counts  [out] NULL, or device uint32[height*width]: M_D (caller-owned).
+ *   out     [out] device fp32[height*width]: the Eq. 7 matrix (caller-owned).
+ *   stream  [in]  cudaStream_t; stream-ordered (host inputs are copied on it first).
+ * Errors: KDE_EINVAL (NULL ctx/x/y/out, n out of range, mixed host/device inputs),
+ *   KDE_EUNSUPPORTED (radial kernel, or a banded context), KDE_ENOMEM, KDE_ECUDA.
+ */
+KDE_API int kde_snap(kde_ctx* c, const double* x, const double* y, const int32_t* label, int64_t n,
+                     uint32_t* counts, float* out, void* stream);
+
 /* Thread-local message describing the last non-OK return on this thread. */
 KDE_API const char* kde_last_error(void);
 

@@ -17,10 +17,10 @@ from ._lib import (KDE_COSINE, KDE_EPANECHNIKOV, KDE_GAUSSIAN, KDE_PATH_DIRECT,
                    KDE_PATH_TENSOR, KDE_PATH_TENSOR_SPLIT, KDE_QUARTIC, KDE_RADIAL, KDE_TRIANGULAR, KDE_TRICUBE,
                    KDE_TRIWEIGHT, KDE_UNIFORM, KERNEL_NAMES, KdeError, kde_create, kde_eval,
                    kde_free, kde_get_bins, kde_get_stats, kde_get_timing, kde_last_error,
-                   kde_load_points, kde_params, kde_set_timing)
+                   kde_load_points, kde_params, kde_set_timing, kde_snap)
 
 __all__ = ["KDE", "KdeError", "kde_params", "kde_create", "kde_load_points", "kde_eval",
-           "kde_get_stats", "kde_get_bins", "kde_set_timing", "kde_get_timing", "kde_last_error",
+           "kde_get_stats", "kde_get_bins", "kde_set_timing", "kde_get_timing", "kde_snap", "kde_last_error",
            "kde_free", "KERNEL_NAMES",
            "KDE_PATH_DIRECT", "KDE_PATH_TENSOR", "KDE_PATH_TENSOR_SPLIT", "KDE_RADIAL", "kernel_id"]
 
@@ -54,6 +54,16 @@ class KDE:
     def load(self, x, y):
         kde_load_points(self.ctx, x, y)
         return self
+
+    def snap(self, x, y, label=None, out=None, counts=None, stream=None):
+        """The paper's own pipeline (Eqs. 5-6 projection, Alg. 3 density matrix with
+        Eqs. 12-13 interpolation, Eq. 7 convolution): returns the (H, W) Eq. 7 matrix."""
+        import torch
+        if out is None:
+            out = torch.empty((self.rows[1] - self.rows[0], self.width), dtype=torch.float32,
+                              device=torch.device("cuda", self.device))
+        kde_snap(self.ctx, x, y, label, out, counts, stream)
+        return out
 
     def eval(self, path="direct", out=None, stream=None):
         import torch

@@ -26,7 +26,7 @@ _CODES = {KDE_EINVAL: "EINVAL", KDE_ENOMEM: "ENOMEM", KDE_ECUDA: "ECUDA",
           KDE_EUNSUPPORTED: "EUNSUPPORTED", KDE_ESTATE: "ESTATE"}
 
 EXPORTS = ("kde_create", "kde_load_points", "kde_eval", "kde_get_stats", "kde_get_bins",
-           "kde_set_timing", "kde_get_timing", "kde_last_error", "kde_free")
+           "kde_set_timing", "kde_get_timing", "kde_snap", "kde_last_error", "kde_free")
 
 
 class kde_params(ctypes.Structure):
@@ -76,10 +76,11 @@ def _load():
     L.kde_last_error.argtypes = []
     L.kde_set_timing.argtypes = [vp, ctypes.c_int]
     L.kde_get_timing.argtypes = [vp, P(kde_timing)]
+    L.kde_snap.argtypes = [vp, vp, vp, vp, ctypes.c_int64, vp, vp, vp]
     L.kde_free.argtypes = [vp]
     L.kde_free.restype = None
     for f in ("kde_create", "kde_load_points", "kde_eval", "kde_get_stats", "kde_get_bins",
-              "kde_set_timing", "kde_get_timing"):
+              "kde_set_timing", "kde_get_timing", "kde_snap"):
         getattr(L, f).restype = ctypes.c_int
     return L
 
@@ -136,6 +137,25 @@ def kde_eval(ctx: int, path: int, out, stream: int | None = None) -> None:
         import torch
         stream = torch.cuda.current_stream(out.device).cuda_stream
     _check(_L.kde_eval(ctx, int(path), _ptr(out), stream))
+
+
+def kde_snap(ctx: int, x, y, label, out, counts=None, stream: int | None = None) -> None:
+    """The paper's snapped pipeline (include/kde.h kde_snap).  x, y: float64, label: int32
+    or None (torch tensors on the context's device, or host tensors / numpy arrays);
+    out: float32 CUDA tensor of H*W; counts: None or an int32/uint32 CUDA tensor of H*W."""
+    n = int(x.shape[0])
+    if int(y.shape[0]) != n or (label is not None and int(label.shape[0]) != n):
+        raise ValueError("x, y and label lengths differ")
+    if str(out.dtype) != "torch.float32" or not out.is_cuda:
+        raise TypeError("out must be a float32 CUDA tensor")
+    if label is not None and str(label.dtype) not in ("int32", "torch.int32"):
+        raise TypeError("labels must be int32")
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream(out.device).cuda_stream
+    _check(_L.kde_snap(ctx, _ptr(x) if n else None, _ptr(y) if n else None,
+                       _ptr(label) if (label is not None and n) else None, n,
+                       _ptr(counts) if counts is not None else None, _ptr(out), stream))
 
 
 def kde_get_stats(ctx: int) -> dict:

@@ -572,6 +572,46 @@ int kde_get_bins(const kde_ctx* c, int64_t* offsets, int64_t* perm, float* lx, f
     return KDE_OK;
 }
 
+int kde_snap(kde_ctx* c, const double* x, const double* y, const int32_t* label, int64_t n,
+             uint32_t* counts, float* out, void* stream) {
+    if (!c || !out || (n > 0 && (!x || !y))) {
+        set_error("kde_snap: NULL argument");
+        return KDE_EINVAL;
+    }
+    if (n < 0 || n > 2147483647ll - 4096) {
+        set_error("kde_snap: n = %lld outside [0, 2^31 - 4097]", (long long)n);
+        return KDE_EINVAL;
+    }
+    if (c->radial) {
+        set_error("kde_snap: Eq. 7's separable window needs a product kernel");
+        return KDE_EUNSUPPORTED;
+    }
+    if (c->g.rb != 0 || c->g.re != c->g.H) {
+        set_error("kde_snap: banded contexts are not supported");
+        return KDE_EUNSUPPORTED;
+    }
+    DeviceGuard dg(c->p.device);
+    if (!dg.ok) return cuda_fail(cudaGetLastError(), "kde_snap: cudaSetDevice");
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "kde_snap: earlier asynchronous error");
+    bool host = false;
+    if (n > 0) {
+        int dx = -1, dy = -1, dl = -1;
+        const bool xd = is_device_ptr(x, &dx), yd = is_device_ptr(y, &dy);
+        const bool ld = label ? is_device_ptr(label, &dl) : xd;
+        if (xd != yd || ld != xd) {
+            set_error("kde_snap: x, y (and label) must all be host or all device pointers");
+            return KDE_EINVAL;
+        }
+        if (xd && (dx != c->p.device || dy != c->p.device || (label && dl != c->p.device))) {
+            set_error("kde_snap: device pointers on another device than the context's");
+            return KDE_EINVAL;
+        }
+        host = !xd;
+    }
+    return snap_run(c, x, y, label, n, counts, out, (cudaStream_t)stream, host);
+}
+
 void kde_free(kde_ctx* c) {
     if (!c) return;
     int prev = -1;
@@ -597,6 +637,7 @@ void kde_free(kde_ctx* c) {
     cudaFree(c->d_stats);
     free_plan(c->plan[0]);
     free_plan(c->plan[1]);
+    snap_free(c);
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     for (int k = 0; k < 2; k++)

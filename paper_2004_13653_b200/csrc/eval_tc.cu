@@ -54,7 +54,7 @@ struct TcArgs {
     float* __restrict__ splat;
     int n;          // MMA N
     int tmem_cols;  // allocated TMEM columns (power of two >= n)
-    float kq, q2, q4;  // Gaussian: -log2(e)/(2 h^2), 2^(2 kq), q2^2
+    float kq, q2;   // Gaussian: -log2(e)/(2 h^2), 2^(2 kq)
     float twoc;     // Cosine: 2 cos(pi / (2 h))
     KConst k;       // 1-D factor constants (kernels.cuh)
 };
@@ -153,63 +153,24 @@ __device__ __forceinline__ void sts128(uint32_t saddr, uint4 v) {
 // residual lo = RN16(f - RN16(f)) into a second operand plane lo_off bytes further, so that
 // A_hi B_hi + A_hi B_lo + A_lo B_hi carries ~22 mantissa bits (the lo*lo term is 2^-22 of
 // the product): the fp32 path's 1e-5 bar on the tensor pipe.
-// Support mask of a unit as fp16x2 AND masks: entry l0*8 + h0 keeps elements l0..h0.
-__device__ __forceinline__ uint4 unit_mask(int l0, int h0) {
-    uint32_t w[4];
-#pragma unroll
-    for (int q = 0; q < 4; q++)
-        w[q] = ((2 * q >= l0 && 2 * q <= h0) ? 0x0000ffffu : 0u) | ((2 * q + 1 >= l0 && 2 * q + 1 <= h0) ? 0xffff0000u : 0u);
-    return make_uint4(w[0], w[1], w[2], w[3]);
-}
-
-__device__ __forceinline__ float2 fmul2(float2 x, float2 y) {  // mul.rn.f32x2: one issue slot
-    unsigned long long r;
-    asm("mul.rn.f32x2 %0, %1, %2;"
-        : "=l"(r)
-        : "l"(*reinterpret_cast<const unsigned long long*>(&x)), "l"(*reinterpret_cast<const unsigned long long*>(&y)));
-    return *reinterpret_cast<float2*>(&r);
-}
-
-__device__ __forceinline__ uint4 lds128(uint32_t saddr) {
-    uint4 v;
-    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(saddr));
-    return v;
-}
-
-// One unit of one operand buffer, warp-wide.  `dirty` (warp-uniform) tracks which of the
-// warp's units of this buffer hold non-zero data from an earlier chunk: a unit that no lane
-// touches and that is already zero is not stored again.
 template <int K, bool SPLIT>
 __device__ __forceinline__ void kern_unit(uint32_t dst, uint32_t lo_off, int c0, float ph, int lo, int span,
-                                          const TcArgs& a, uint32_t mtab, uint32_t& dirty, uint32_t bit) {
+                                          const TcArgs& a) {
     const int l0 = max(lo - c0, 0), h0 = min(lo + span - c0, 7);
-    const bool ne = l0 <= h0;
-    const bool any = __any_sync(0xffffffffu, ne);
-    if (!any && !(dirty & bit)) return;
-    dirty = any ? (dirty | bit) : (dirty & ~bit);
     uint4 o = make_uint4(0u, 0u, 0u, 0u);
     uint4 ol = make_uint4(0u, 0u, 0u, 0u);
-    if (ne) {
+    if (l0 <= h0) {
+        const uint32_t m = (2u << h0) - (1u << l0);
         const float d0 = (float)c0 - ph;
         float f[8];
         if constexpr (K == KDE_GAUSSIAN) {
-            // g(d+1) = g(d) r(d), r(d+1) = r(d) q^2, two elements per packed multiply:
-            // (f[e+2], f[e+3]) = (f[e], f[e+1]) * (r_e r_{e+1}, r_{e+1} r_{e+2}), whose next
-            // value is this one * (q^4, q^4)
-            const float g0 = ex2_ftz(d0 * d0 * a.kq);
-            const float r0 = ex2_ftz(fmaf(2.0f, d0, 1.0f) * a.kq);
-            const float rr = r0 * r0;
-            float2 v = make_float2(g0, g0 * r0);
-            float2 w = fmul2(make_float2(rr, rr), make_float2(a.q2, a.q2 * a.q2 * a.q2));
-            const float2 q4 = make_float2(a.q4, a.q4);
-            f[0] = v.x;
-            f[1] = v.y;
+            float gv = ex2_ftz(d0 * d0 * a.kq);
+            float r = ex2_ftz(fmaf(2.0f, d0, 1.0f) * a.kq);
 #pragma unroll
-            for (int e = 2; e < 8; e += 2) {
-                v = fmul2(v, w);
-                if (e < 6) w = fmul2(w, q4);
-                f[e] = v.x;
-                f[e + 1] = v.y;
+            for (int e = 0; e < 8; e++) {
+                f[e] = gv;
+                gv *= r;
+                r *= a.q2;
             }
         } else if constexpr (K == KDE_COSINE) {
             f[0] = __cosf(d0 * a.k.kc);
@@ -222,17 +183,17 @@ __device__ __forceinline__ void kern_unit(uint32_t dst, uint32_t lo_off, int c0,
 #pragma unroll
             for (int e = 0; e < 8; e++) f[e] = khat<K>(d0 + (float)e, a.k);
         }
-        const uint4 m = lds128(mtab + (uint32_t)(l0 * 8 + h0) * 16u);
-        o = make_uint4(pack_half2(f[0], f[1]) & m.x, pack_half2(f[2], f[3]) & m.y,
-                       pack_half2(f[4], f[5]) & m.z, pack_half2(f[6], f[7]) & m.w);
+#pragma unroll
+        for (int e = 0; e < 8; e++) f[e] = (m & (1u << e)) ? f[e] : 0.f;
+        o = make_uint4(pack_half2(f[0], f[1]), pack_half2(f[2], f[3]), pack_half2(f[4], f[5]),
+                       pack_half2(f[6], f[7]));
         if constexpr (SPLIT) {
             const uint32_t hw[4] = {o.x, o.y, o.z, o.w};
-            const uint32_t mw[4] = {m.x, m.y, m.z, m.w};
             uint32_t lw[4];
 #pragma unroll
             for (int q = 0; q < 4; q++) {
                 const float2 hv = __half22float2(*reinterpret_cast<const __half2*>(&hw[q]));
-                lw[q] = pack_half2(f[2 * q] - hv.x, f[2 * q + 1] - hv.y) & mw[q];
+                lw[q] = pack_half2(f[2 * q] - hv.x, f[2 * q + 1] - hv.y);
             }
             ol = make_uint4(lw[0], lw[1], lw[2], lw[3]);
         }
@@ -251,7 +212,6 @@ __global__ void __launch_bounds__(kTcThreads, TcShape<H>::kMinBlocks) tc_splat_k
     __shared__ uint32_t s_tmem;
     __shared__ int s_w;
     __shared__ uint32_t s_pre[kMaxStack + 1];   // first sorted position of each stack bucket
-    __shared__ uint4 s_mtab[64];                // unit support masks (unit_mask)
 
     const Geom& g = a.g;
     const PathGeom& pg = a.pg;
@@ -269,7 +229,6 @@ __global__ void __launch_bounds__(kTcThreads, TcShape<H>::kMinBlocks) tc_splat_k
                      "r"(a.tmem_cols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    if (t < 64) s_mtab[t] = unit_mask(t >> 3, t & 7);
     if (t == 0) {
         mbar_init(&s_bar[0], 1);
         mbar_init(&s_bar[1], 1);
@@ -281,7 +240,6 @@ __global__ void __launch_bounds__(kTcThreads, TcShape<H>::kMinBlocks) tc_splat_k
     tc_fence_after();
     const uint32_t tmem = s_tmem;
     uint32_t nuse[2] = {0u, 0u};  // commits issued per operand buffer (same on all threads)
-    uint64_t dirty = ~0ull;       // per buffer (32 bits each): this warp's units holding non-zero data
     uint32_t nacc = 0;            // accumulator-ready commits
 
     // A buffer b at sm_a + b * astride (SPLIT: its lo plane kTcABytes further), B buffer b
@@ -373,22 +331,17 @@ __global__ void __launch_bounds__(kTcThreads, TcShape<H>::kMinBlocks) tc_splat_k
             if (nuse[b] > 0) mbar_wait(&s_bar[b], (nuse[b] - 1) & 1);
             const uint32_t ab = sm_a + b * astride + koff;
             const uint32_t bb = sm_b + b * bstride + koff;
-            const uint32_t mtab = smem_u32(s_mtab);
-            uint32_t db = (uint32_t)(dirty >> (32 * b));  // bits: A units j*H + h, B units 16 + k*H + h
 #pragma unroll
             for (int j = 0; j < kTcM / 32; j++) {  // A: 16 row units, 4 per warp
                 const int u = warp + 4 * j;
 #pragma unroll
                 for (int h = 0; h < H; h++)
-                    kern_unit<K, SPLIT>(ab + u * kSBO + h * 512, kTcABytes, u * 8, pyh[h], jlo[h], jspan[h], a,
-                                        mtab, db, 1u << (j * H + h));
+                    kern_unit<K, SPLIT>(ab + u * kSBO + h * 512, kTcABytes, u * 8, pyh[h], jlo[h], jspan[h], a);
             }
-            for (int u = warp, k = 0; u < nbu; u += 4, k++)  // B: N/8 column units
+            for (int u = warp; u < nbu; u += 4)  // B: N/8 column units
 #pragma unroll
                 for (int h = 0; h < H; h++)
-                    kern_unit<K, SPLIT>(bb + u * kSBO + h * 512, bbytes, u * 8, pxh[h], ilo[h], ispan[h], a,
-                                        mtab, db, 1u << (16 + k * H + h));
-            dirty = b ? ((dirty & 0xffffffffull) | ((uint64_t)db << 32)) : ((dirty & ~0xffffffffull) | db);
+                    kern_unit<K, SPLIT>(bb + u * kSBO + h * 512, bbytes, u * 8, pxh[h], ilo[h], ispan[h], a);
             fence_async_smem();
             __syncthreads();
             if (t == kIssuer) {  // warp 3 generates the fewest B units
@@ -478,7 +431,6 @@ int launch_tc(kde_ctx* c, float* out, cudaStream_t s, bool split) {
     while (a.tmem_cols < a.n) a.tmem_cols <<= 1;
     a.kq = (float)(-0.5 * 1.4426950408889634074 / (c->hpx * c->hpx));
     a.q2 = (float)exp2(2.0 * (double)a.kq);
-    a.q4 = (float)exp2(4.0 * (double)a.kq);
     a.twoc = (float)(2.0 * cos(3.14159265358979323846 / (2.0 * c->hpx)));
     a.k = make_kconst(c->hpx);
     // chunk_pts is 32 (H = 1): 64-point chunks measured slower

@@ -83,6 +83,17 @@ struct PathGeom {
     __host__ __device__ int64_t slot_floats() const { return (int64_t)slot_w * slot_h; }
 };
 
+// Buffers of the snapped pipeline (kde_snap, snap.cu), allocated on first use.
+struct SnapBufs {
+    int64_t cap = 0;                 // staging capacity (points) for host inputs
+    double *x = nullptr, *y = nullptr;
+    int32_t* lab = nullptr;
+    uint32_t* counts = nullptr;      // M_D when the caller passes no counts buffer
+    float* tmp = nullptr;            // Eq. 7 row pass
+    unsigned long long* ext = nullptr;  // encoded x/y extent
+    float* w = nullptr;              // 1-D weights
+};
+
 struct EvalPlan {
     PathGeom pg;
     bool enabled = false;
@@ -157,6 +168,7 @@ struct kde_ctx {
     cudaEvent_t tev[6] = {};                   // bin0, bin1 (load); plan0, main0, main1, comb1 (eval)
     bool tev_load = false, tev_eval = false;
     kde::EvalPlan plan[2];                     // [KDE_PATH_DIRECT], [KDE_PATH_TENSOR]
+    kde::SnapBufs snap;                        // kde_snap (NEXT-F1)
 };
 
 namespace kde {
@@ -176,5 +188,9 @@ int launch_tc(kde_ctx* c, float* out, cudaStream_t s, bool split);
 int plan_device(kde_ctx* c, EvalPlan& pl, cudaStream_t s);
 int plan_nblk(const PathGeom& pg);
 int launch_combine(kde_ctx* c, const EvalPlan& pl, float* out, cudaStream_t s);
+// snapped pipeline (snap.cu)
+int snap_run(kde_ctx* c, const double* x, const double* y, const int32_t* label, int64_t n,
+             uint32_t* counts, float* out, cudaStream_t s, bool host);
+void snap_free(kde_ctx* c);
 
 }  // namespace kde
