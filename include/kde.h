@@ -240,6 +240,29 @@ KDE_API int kde_get_timing(kde_ctx* c, kde_timing* t);
 KDE_API int kde_snap(kde_ctx* c, const double* x, const double* y, const int32_t* label, int64_t n,
                      uint32_t* counts, float* out, void* stream);
 
+/*
+ * kde_dp: GPU Douglas-Peucker compression of a batch of trajectories (SURVEY.md §8f
+ * NEXT-F3; PAPER.md:116-129 serial DP, §IV-A P:184-331 its GPU parallelisation), the
+ * producer of the north star's "DP-compressed" inputs.  Level-synchronous: every round
+ * computes the VED (Eq. 9, fp64, one rounding per operation) of every
+ * unretained point to its current chord, keeps the earliest point of maximal VED of every
+ * segment whose maximum is strictly larger than eps, and splits the segment there;
+ * it stops when a round keeps nothing.  The kept set equals the serial recursion's
+ * (R14: strict >, earliest index on ties, degenerate chord -> point distance).
+ *   x, y          [in]  n fp64 coordinates (n = traj_offsets[ntraj]), all trajectories
+ *                       concatenated (the paper's merged store, TLen)
+ *   traj_offsets  [in]  ntraj + 1 int64, nondecreasing, traj_offsets[0] = 0
+ *   ntraj         [in]  >= 0
+ *   eps           [in]  threshold, finite, >= 0 (same units as x, y)
+ *   keep          [out] n uint8: 1 = retained (end points always)
+ *   device        [in]  CUDA ordinal; stream [in] cudaStream_t
+ *   n_kept, rounds [out] NULL or host int64: retained count, rounds run
+ * Pointers: all device (on `device`) or all host (staged through the device).
+ * Synchronous (one 4-byte readback per 4 rounds).  Errors: KDE_EINVAL, KDE_ENOMEM, KDE_ECUDA.
+ */
+KDE_API int kde_dp(const double* x, const double* y, const int64_t* traj_offsets, int64_t ntraj, double eps,
+                   uint8_t* keep, int32_t device, void* stream, int64_t* n_kept, int64_t* rounds);
+
 /* Thread-local message describing the last non-OK return on this thread. */
 KDE_API const char* kde_last_error(void);
 

@@ -26,7 +26,7 @@ _CODES = {KDE_EINVAL: "EINVAL", KDE_ENOMEM: "ENOMEM", KDE_ECUDA: "ECUDA",
           KDE_EUNSUPPORTED: "EUNSUPPORTED", KDE_ESTATE: "ESTATE"}
 
 EXPORTS = ("kde_create", "kde_load_points", "kde_eval", "kde_get_stats", "kde_get_bins",
-           "kde_set_timing", "kde_get_timing", "kde_snap", "kde_last_error", "kde_free")
+           "kde_set_timing", "kde_get_timing", "kde_snap", "kde_dp", "kde_last_error", "kde_free")
 
 
 class kde_params(ctypes.Structure):
@@ -77,10 +77,12 @@ def _load():
     L.kde_set_timing.argtypes = [vp, ctypes.c_int]
     L.kde_get_timing.argtypes = [vp, P(kde_timing)]
     L.kde_snap.argtypes = [vp, vp, vp, vp, ctypes.c_int64, vp, vp, vp]
+    L.kde_dp.argtypes = [vp, vp, vp, ctypes.c_int64, ctypes.c_double, vp, ctypes.c_int32, vp,
+                         P(ctypes.c_int64), P(ctypes.c_int64)]
     L.kde_free.argtypes = [vp]
     L.kde_free.restype = None
     for f in ("kde_create", "kde_load_points", "kde_eval", "kde_get_stats", "kde_get_bins",
-              "kde_set_timing", "kde_get_timing", "kde_snap"):
+              "kde_set_timing", "kde_get_timing", "kde_snap", "kde_dp"):
         getattr(L, f).restype = ctypes.c_int
     return L
 
@@ -156,6 +158,29 @@ def kde_snap(ctx: int, x, y, label, out, counts=None, stream: int | None = None)
     _check(_L.kde_snap(ctx, _ptr(x) if n else None, _ptr(y) if n else None,
                        _ptr(label) if (label is not None and n) else None, n,
                        _ptr(counts) if counts is not None else None, _ptr(out), stream))
+
+
+def kde_dp(x, y, traj_offsets, eps: float, keep=None, device: int = 0, stream: int | None = None):
+    """GPU Douglas-Peucker (include/kde.h kde_dp).  x, y float64 and traj_offsets int64:
+    CUDA tensors on `device` (keep: a uint8 CUDA tensor, allocated if None) or host
+    arrays/tensors (keep: a host uint8 array).  Returns (keep, n_kept, rounds)."""
+    n = int(x.shape[0])
+    ntraj = int(traj_offsets.shape[0]) - 1
+    dev = not isinstance(x, np.ndarray) and x.is_cuda
+    if keep is None:
+        if dev:
+            import torch
+            keep = torch.empty(n, dtype=torch.uint8, device=x.device)
+        else:
+            keep = np.zeros(n, np.uint8)
+    if stream is None and dev:
+        import torch
+        stream = torch.cuda.current_stream(x.device).cuda_stream
+    nk, rounds = ctypes.c_int64(0), ctypes.c_int64(0)
+    _check(_L.kde_dp(_ptr(x) if n else None, _ptr(y) if n else None, _ptr(traj_offsets), ntraj,
+                     float(eps), _ptr(keep) if n else None, int(device), stream,
+                     ctypes.byref(nk), ctypes.byref(rounds)))
+    return keep, nk.value, rounds.value
 
 
 def kde_get_stats(ctx: int) -> dict:

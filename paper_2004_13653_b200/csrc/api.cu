@@ -612,6 +612,83 @@ int kde_snap(kde_ctx* c, const double* x, const double* y, const int32_t* label,
     return snap_run(c, x, y, label, n, counts, out, (cudaStream_t)stream, host);
 }
 
+int kde_dp(const double* x, const double* y, const int64_t* traj_offsets, int64_t ntraj, double eps,
+           uint8_t* keep, int32_t device, void* stream, int64_t* n_kept, int64_t* rounds) {
+    if (ntraj < 0 || !(eps >= 0.0) || !isfinite(eps)) {
+        set_error("kde_dp: ntraj = %lld, eps = %g (need ntraj >= 0, finite eps >= 0)", (long long)ntraj, eps);
+        return KDE_EINVAL;
+    }
+    if (!traj_offsets) {
+        set_error("kde_dp: NULL traj_offsets");
+        return KDE_EINVAL;
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        set_error("kde_dp: no CUDA device %d (no CPU fallback exists)", device);
+        return KDE_ECUDA;
+    }
+    DeviceGuard dg(device);
+    if (!dg.ok) return cuda_fail(cudaGetLastError(), "kde_dp: cudaSetDevice");
+    cudaStream_t s = (cudaStream_t)stream;
+    int dd = -1;
+    const bool dev = is_device_ptr(traj_offsets, &dd);
+    int64_t n = 0;
+    if (dev) {
+        if (cudaMemcpyAsync(&n, traj_offsets + ntraj, sizeof n, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            return cuda_fail(cudaGetLastError(), "kde_dp: offsets readback");
+    } else {
+        n = traj_offsets[ntraj];
+    }
+    if (n < 0 || n > 2147483647ll - 4096) {
+        set_error("kde_dp: %lld points outside [0, 2^31 - 4097]", (long long)n);
+        return KDE_EINVAL;
+    }
+    if (n_kept) *n_kept = 0;
+    if (rounds) *rounds = 0;
+    if (n == 0) return KDE_OK;
+    if (!x || !y || !keep) {
+        set_error("kde_dp: NULL x, y or keep");
+        return KDE_EINVAL;
+    }
+    int d1 = -1, d2 = -1, d3 = -1;
+    if (is_device_ptr(x, &d1) != dev || is_device_ptr(y, &d2) != dev || is_device_ptr(keep, &d3) != dev) {
+        set_error("kde_dp: x, y, traj_offsets and keep must all be host or all device pointers");
+        return KDE_EINVAL;
+    }
+    if (dev) return dp_run(x, y, traj_offsets, (int)ntraj, (int)n, eps, keep, s, n_kept, rounds);
+    // host inputs: stage on the device, copy the mask back
+    double *dx = nullptr, *dy = nullptr;
+    int64_t* doff = nullptr;
+    uint8_t* dk = nullptr;
+    cudaError_t e = cudaMalloc(&dx, sizeof(double) * n);
+    if (e == cudaSuccess) e = cudaMalloc(&dy, sizeof(double) * n);
+    if (e == cudaSuccess) e = cudaMalloc(&doff, sizeof(int64_t) * (ntraj + 1));
+    if (e == cudaSuccess) e = cudaMalloc(&dk, n);
+    int rc = KDE_OK;
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        set_error("kde_dp: staging allocation failed");
+        rc = KDE_ENOMEM;
+    } else {
+        cudaMemcpyAsync(dx, x, sizeof(double) * n, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(dy, y, sizeof(double) * n, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(doff, traj_offsets, sizeof(int64_t) * (ntraj + 1), cudaMemcpyHostToDevice, s);
+        rc = dp_run(dx, dy, doff, (int)ntraj, (int)n, eps, dk, s, n_kept, rounds);
+        if (rc == KDE_OK) {
+            e = cudaMemcpyAsync(keep, dk, n, cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+            if (e != cudaSuccess) rc = cuda_fail(e, "kde_dp: mask readback");
+        }
+    }
+    cudaFree(dx);
+    cudaFree(dy);
+    cudaFree(doff);
+    cudaFree(dk);
+    return rc;
+}
+
 void kde_free(kde_ctx* c) {
     if (!c) return;
     int prev = -1;

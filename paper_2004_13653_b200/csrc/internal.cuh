@@ -192,5 +192,8 @@ int launch_combine(kde_ctx* c, const EvalPlan& pl, float* out, cudaStream_t s);
 int snap_run(kde_ctx* c, const double* x, const double* y, const int32_t* label, int64_t n,
              uint32_t* counts, float* out, cudaStream_t s, bool host);
 void snap_free(kde_ctx* c);
+// GPU Douglas-Peucker (dp.cu); device pointers
+int dp_run(const double* x, const double* y, const int64_t* offs, int ntraj, int n, double eps, uint8_t* keep,
+           cudaStream_t s, int64_t* n_kept, int64_t* rounds);
 
 }  // namespace kde

@@ -77,22 +77,43 @@ __global__ void __launch_bounds__(kSnapThreads) snap_project_kernel(
     const double* __restrict__ x, const double* __restrict__ y, const int32_t* __restrict__ label, int n,
     const unsigned long long* __restrict__ ext, int u, int v, uint32_t* __restrict__ M) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const double xa = x[i], ya = y[i];
-    if (!isfinite(xa) || !isfinite(ya)) return;
+    const int lane = threadIdx.x & 31;
     const double x0 = unord64(ext[0]), x1 = unord64(ext[1]);
     const double y0 = unord64(ext[2]), y1 = unord64(ext[3]);
-    const int cx = snap_cell(xa, x0, x1, u), cy = snap_cell(ya, y0, y1, v);
-    atomicAdd(&M[(size_t)(cy - 1) * u + (cx - 1)], 1u);  // Alg. 3 step 2
-    if (!label || i + 1 >= n || label[i] != label[i + 1]) return;
-    const double xb = x[i + 1], yb = y[i + 1];
-    if (!isfinite(xb) || !isfinite(yb)) return;
-    const int dx = snap_cell(xb, x0, x1, u) - cx, dy = snap_cell(yb, y0, y1, v) - cy;
-    const int cmax = max(abs(dx), abs(dy));
-    for (int c = 1; c < cmax; c++) {  // Eqs. 12-13, c = 1 .. c_max - 1 (R18)
-        const int ix = cx + round_half_up_ratio(c * dx, cmax);
-        const int iy = cy + round_half_up_ratio(c * dy, cmax);
-        atomicAdd(&M[(size_t)(iy - 1) * u + (ix - 1)], 1u);
+    int cx = 0, cy = 0, dx = 0, dy = 0, cmax = 0;  // cmax > 1: this point opens a gap
+    if (i < n) {
+        const double xa = x[i], ya = y[i];
+        if (isfinite(xa) && isfinite(ya)) {
+            cx = snap_cell(xa, x0, x1, u);
+            cy = snap_cell(ya, y0, y1, v);
+            atomicAdd(&M[(size_t)(cy - 1) * u + (cx - 1)], 1u);  // Alg. 3 step 2
+            if (label && i + 1 < n && label[i] == label[i + 1]) {
+                const double xb = x[i + 1], yb = y[i + 1];
+                if (isfinite(xb) && isfinite(yb)) {
+                    dx = snap_cell(xb, x0, x1, u) - cx;
+                    dy = snap_cell(yb, y0, y1, v) - cy;
+                    cmax = max(abs(dx), abs(dy));
+                }
+            }
+        }
+    }
+    // Eqs. 12-13, c = 1 .. c_max - 1 (R18): short gaps by their own lane, long ones (AIS
+    // reports up to 180 s apart span hundreds of cells) by the whole warp
+    const bool big = cmax > 32;
+    if (!big)
+        for (int c = 1; c < cmax; c++)
+            atomicAdd(&M[(size_t)(cy + round_half_up_ratio(c * dy, cmax) - 1) * u +
+                         (cx + round_half_up_ratio(c * dx, cmax) - 1)], 1u);
+    unsigned m = __ballot_sync(0xffffffffu, big);
+    while (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        const int gx = __shfl_sync(0xffffffffu, cx, src), gy = __shfl_sync(0xffffffffu, cy, src);
+        const int gdx = __shfl_sync(0xffffffffu, dx, src), gdy = __shfl_sync(0xffffffffu, dy, src);
+        const int gm = __shfl_sync(0xffffffffu, cmax, src);
+        for (int c = 1 + lane; c < gm; c += 32)
+            atomicAdd(&M[(size_t)(gy + round_half_up_ratio(c * gdy, gm) - 1) * u +
+                         (gx + round_half_up_ratio(c * gdx, gm) - 1)], 1u);
     }
 }
 

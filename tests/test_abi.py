@@ -8,6 +8,7 @@ import ctypes
 import os
 import re
 
+import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -102,6 +103,9 @@ def test_null_arguments_are_einval():
     assert L.kde_eval(None, 0, None, None) == _lib.KDE_EINVAL
     assert L.kde_get_stats(None, None) == _lib.KDE_EINVAL
     assert L.kde_get_bins(None, None, None, None, None, None) == _lib.KDE_EINVAL
+    assert L.kde_snap(None, None, None, None, 0, None, None, None) == _lib.KDE_EINVAL
+    assert L.kde_dp(None, None, None, 0, 1.0, None, 0, None, None, None) == _lib.KDE_EINVAL
+    assert L.kde_dp(None, None, None, -1, 1.0, None, 0, None, None, None) == _lib.KDE_EINVAL
     L.kde_free(None)  # NULL-safe
 
 
@@ -112,4 +116,8 @@ def test_no_device_fails_loudly_without_fallback():
     from paper_2004_13653_b200 import _lib
     with pytest.raises(_lib.KdeError) as e:
         _lib.kde_create(_params())
+    assert e.value.code == _lib.KDE_ECUDA
+    x = np.linspace(0.0, 1.0, 8)
+    with pytest.raises(_lib.KdeError) as e:  # the GPU Douglas-Peucker has no CPU fallback either
+        _lib.kde_dp(x, x, np.array([0, 8], np.int64), 0.1)
     assert e.value.code == _lib.KDE_ECUDA
