@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) splat_kernel(const SplatArgs a
 
 // Segment reduce: for every split group (listed by the planner) and sub-window, the
 // segment blocks are summed IN SEGMENT ORDER into segment 0's slot.  One CTA per
-// (group x sub-window, 1024-float chunk of the slot); float4, 4 segments in flight.
+// (group x sub-window, 1024-float chunk of the slot); float4, 8 segments in flight.
 __global__ void __launch_bounds__(256) segreduce_kernel(const int* __restrict__ hot,
                                                         const int* __restrict__ totals,
                                                         const int2* __restrict__ group, int nsub,
@@ -318,22 +318,31 @@ __global__ void __launch_bounds__(256) segreduce_kernel(const int* __restrict__ 
         const int2 gr = group[hot[gsub / nsub]];
         const int sub = gsub % nsub;
         float* d0 = splat + ((size_t)gr.x * nsub + sub) * slot_floats + e;
-        float4 acc = *reinterpret_cast<const float4*>(d0);
+        // 8 loads in flight, 4 partial sums (segment k goes to partial k mod 4 within each
+        // group of 8), combined pairwise: a fixed order, so the result is deterministic and
+        // band-invariant; the dependent-load chain of the hottest group is n/8 long
+        float4 p[4] = {*reinterpret_cast<const float4*>(d0), make_float4(0.f, 0.f, 0.f, 0.f),
+                       make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
         int k = 1;
-        for (; k + 4 <= gr.y; k += 4) {
-            const float4 v0 = *reinterpret_cast<const float4*>(d0 + k * stride);
-            const float4 v1 = *reinterpret_cast<const float4*>(d0 + (k + 1) * stride);
-            const float4 v2 = *reinterpret_cast<const float4*>(d0 + (k + 2) * stride);
-            const float4 v3 = *reinterpret_cast<const float4*>(d0 + (k + 3) * stride);
-            acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
-            acc.x += v1.x; acc.y += v1.y; acc.z += v1.z; acc.w += v1.w;
-            acc.x += v2.x; acc.y += v2.y; acc.z += v2.z; acc.w += v2.w;
-            acc.x += v3.x; acc.y += v3.y; acc.z += v3.z; acc.w += v3.w;
+        for (; k + 8 <= gr.y; k += 8) {
+            float4 v[8];
+#pragma unroll
+            for (int q = 0; q < 8; q++) v[q] = *reinterpret_cast<const float4*>(d0 + (k + q) * stride);
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                float4& t = p[q & 3];
+                t.x += v[q].x; t.y += v[q].y; t.z += v[q].z; t.w += v[q].w;
+            }
         }
         for (; k < gr.y; k++) {
             const float4 v = *reinterpret_cast<const float4*>(d0 + k * stride);
-            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+            p[0].x += v.x; p[0].y += v.y; p[0].z += v.z; p[0].w += v.w;
         }
+        float4 acc;
+        acc.x = (p[0].x + p[1].x) + (p[2].x + p[3].x);
+        acc.y = (p[0].y + p[1].y) + (p[2].y + p[3].y);
+        acc.z = (p[0].z + p[1].z) + (p[2].z + p[3].z);
+        acc.w = (p[0].w + p[1].w) + (p[2].w + p[3].w);
         *reinterpret_cast<float4*>(d0) = acc;
     }
 }
