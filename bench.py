@@ -206,6 +206,8 @@ def run_ours(args):
     launches = k.stats()["kernel_launches"] - launches0
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms = sum(step_ms) / len(step_ms)
+    step_stats = {"mean": round(ms, 4), "median": round(statistics.median(step_ms), 4),
+                  "min": round(min(step_ms), 4)}
 
     # --- per-phase device times (CUDA events recorded by libkde on the streams its
     # kernels run on), for the dominant kernel's roofline
@@ -317,6 +319,7 @@ def run_ours(args):
                    "l2": "flushed (512 MiB write) before every timed step"},
         "pixels_per_s": W * H / (ms * 1e-3),
         "useful_pairs": useful,
+        "step_ms_rank0": step_stats,
         "e2e": {"value": useful / (e2e * 1e-3), "unit": UNIT, "ms_per_step": round(e2e, 4),
                 "h2d_bytes_per_step": 16 * cfg["n"],
                 "d2h_bytes_per_step": 4 * W * H,

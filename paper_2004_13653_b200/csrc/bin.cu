@@ -403,7 +403,14 @@ int bin_points(kde_ctx* c, const double* d_x, const double* d_y, int64_t n64) {
     const int dbits = (bits + passes - 1) / passes;
     const uint32_t dmask = (1u << dbits) - 1u;
     const int nbins = (int)dmask + 1;
-    const int rounds = rs_rounds(nbins);
+    // tuning knobs (A/B experiments): KDE_RS_ROUNDS = 8|16 forces the tile rounds,
+    // KDE_RS_STAGED = the largest digit count that stages the tile in shared memory
+    static const int env_rounds = getenv("KDE_RS_ROUNDS") ? atoi(getenv("KDE_RS_ROUNDS")) : 0;
+    static const int env_staged = getenv("KDE_RS_STAGED") ? atoi(getenv("KDE_RS_STAGED")) : 256;
+    // default: 4096-key tiles from 8 M points on (measured: C4 binning 0.96 -> 0.91 ms; C2
+    // prefers 2048-key tiles: more CTAs for its 2 M keys)
+    const int rounds = (env_rounds == 8 || env_rounds == 16) ? std::max(env_rounds, nbins / 64)
+                       : (n >= (8 << 20) ? std::max(16, nbins / 64) : rs_rounds(nbins));
     const int tile = kRsThreads * rounds;
     const int nblk = (n + tile - 1) / tile;
     if (n64 > pb.cap || pb.key[0] == nullptr) {
@@ -430,16 +437,16 @@ int bin_points(kde_ctx* c, const double* d_x, const double* d_y, int64_t n64) {
         const size_t up_smem = sizeof(uint32_t) * nbins;
         // small digit sets scatter short runs: stage the tile digit-sorted in shared memory
         // and write it out coalesced; large ones (>= 512 digits) scatter directly
-        const bool staged = nbins < 512;
+        const bool staged = nbins <= env_staged;
         const size_t dn_smem =
             sizeof(uint32_t) * (2 * nbins + (staged ? 2 * tile : 0)) + sizeof(uint16_t) * 8 * nbins;
         static bool attr = false;
-        if (!attr) {  // largest cases: staged 256 digits x tile 2048; direct 1024 digits
-            const int st = (int)(sizeof(uint32_t) * (2 * 256 + 2 * 2048) + sizeof(uint16_t) * 8 * 256);
-            const int dr = (int)(sizeof(uint32_t) * 2 * 1024 + sizeof(uint16_t) * 8 * 1024);
-            cudaFuncSetAttribute(rs_downsweep<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, st);
-            cudaFuncSetAttribute(rs_downsweep<false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, dr);
-            cudaFuncSetAttribute(rs_downsweep<false, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, dr);
+        if (!attr) {  // largest case: 1024 digits, tile 4096, staged
+            const int mx = (int)(sizeof(uint32_t) * (2 * 1024 + 2 * 4096) + sizeof(uint16_t) * 8 * 1024);
+            cudaFuncSetAttribute(rs_downsweep<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+            cudaFuncSetAttribute(rs_downsweep<true, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+            cudaFuncSetAttribute(rs_downsweep<false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+            cudaFuncSetAttribute(rs_downsweep<false, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
             attr = true;
         }
         bin_convert_kernel<<<nblk, kRsThreads, up_smem, s>>>(d_x, d_y, n, g, nb, pb.key[0], pb.rec,
@@ -453,7 +460,8 @@ int bin_points(kde_ctx* c, const double* d_x, const double* d_y, int64_t n64) {
                 c->launches += 1;
             }
             rs_scan_digits<<<nbins, 256, 0, s>>>(pb.hist, nbins, nblk, pb.scan_tmp);
-            auto dsw = staged ? rs_downsweep<true, 8> : (rounds == 8 ? rs_downsweep<false, 8> : rs_downsweep<false, 16>);
+            auto dsw = staged ? (rounds == 8 ? rs_downsweep<true, 8> : rs_downsweep<true, 16>)
+                              : (rounds == 8 ? rs_downsweep<false, 8> : rs_downsweep<false, 16>);
             dsw<<<nblk, kRsThreads, dn_smem, s>>>(pb.key[cur], ps == 0 ? nullptr : pb.val[cur], pb.key[cur ^ 1],
                                                   pb.val[cur ^ 1], n, shift, dmask, pb.hist, pb.scan_tmp, nblk);
             c->launches += 2;

@@ -21,7 +21,7 @@
 namespace kde {
 
 constexpr int kPlanThreads = 256;
-constexpr int kPlanPer = 4;  // groups per thread
+constexpr int kPlanPer = 1;  // groups per thread (more CTAs: the plan is latency-bound)
 constexpr int kPlanTile = kPlanThreads * kPlanPer;
 
 // Bucket keys are column-major (key = bx * nby + by), so a group -- a vertical stack of
@@ -89,24 +89,22 @@ __global__ void __launch_bounds__(kPlanThreads) plan_local_kernel(const Geom g, 
     if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
 }
 
-// one CTA: exclusive scan of the block totals, in place; bsum[nblk] = grand total
+// one CTA: exclusive scan of the block totals, in place; bsum[nblk] = grand total.  Each
+// thread owns a run of consecutive totals (sequential), one block scan joins the runs.
 __global__ void __launch_bounds__(kPlanThreads) plan_blocks_kernel(uint64_t* __restrict__ bsum, int nblk) {
     __shared__ uint64_t s_warp[kPlanThreads / 32];
-    __shared__ uint64_t s_carry;
-    if (threadIdx.x == 0) s_carry = 0;
-    __syncthreads();
-    for (int b0 = 0; b0 < nblk; b0 += kPlanThreads) {
-        const int b = b0 + threadIdx.x;
-        const uint64_t v = b < nblk ? bsum[b] : 0;
-        uint64_t tot;
-        const uint64_t ex = block_scan_u64(v, s_warp, &tot);
-        const uint64_t carry = s_carry;
-        if (b < nblk) bsum[b] = carry + ex;
-        __syncthreads();
-        if (threadIdx.x == 0) s_carry = carry + tot;
-        __syncthreads();
+    const int per = (nblk + kPlanThreads - 1) / kPlanThreads;
+    const int b0 = threadIdx.x * per, b1 = min(b0 + per, nblk);
+    uint64_t sum = 0;
+    for (int b = b0; b < b1; b++) sum += bsum[b];
+    uint64_t tot;
+    uint64_t run = block_scan_u64(sum, s_warp, &tot);
+    for (int b = b0; b < b1; b++) {
+        const uint64_t v = bsum[b];
+        bsum[b] = run;
+        run += v;
     }
-    if (threadIdx.x == 0) bsum[nblk] = s_carry;
+    if (threadIdx.x == 0) bsum[nblk] = tot;
 }
 
 __global__ void __launch_bounds__(kPlanThreads) plan_finish_kernel(

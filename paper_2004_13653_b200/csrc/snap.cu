@@ -52,11 +52,24 @@ __global__ void __launch_bounds__(kSnapThreads) snap_extent_kernel(const double*
             mn[k] = min(mn[k], __shfl_xor_sync(0xffffffffu, mn[k], o));
             mx[k] = max(mx[k], __shfl_xor_sync(0xffffffffu, mx[k], o));
         }
-    if ((threadIdx.x & 31) == 0 && mx[0] != 0ull) {
-        atomicMin(&ext[0], mn[0]);
-        atomicMax(&ext[1], mx[0]);
-        atomicMin(&ext[2], mn[1]);
-        atomicMax(&ext[3], mx[1]);
+    __shared__ unsigned long long s_r[4][kSnapThreads / 32];  // per warp, then one atomic per CTA
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        s_r[0][w] = mn[0];
+        s_r[1][w] = mx[0];
+        s_r[2][w] = mn[1];
+        s_r[3][w] = mx[1];
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        const int k = threadIdx.x;
+        unsigned long long r = s_r[k][0];
+        for (int q = 1; q < kSnapThreads / 32; q++) r = (k & 1) ? max(r, s_r[k][q]) : min(r, s_r[k][q]);
+        const bool any = (k & 1) ? r != 0ull : r != ~0ull;
+        if (any) {
+            if (k & 1) atomicMax(&ext[k], r);
+            else atomicMin(&ext[k], r);
+        }
     }
 }
 
@@ -253,7 +266,7 @@ int snap_run(kde_ctx* c, const double* x, const double* y, const int32_t* label,
     cudaMemcpyAsync(sb.ext, init, sizeof init, cudaMemcpyHostToDevice, s);
     cudaMemsetAsync(counts, 0, sizeof(uint32_t) * npx, s);
     if (n > 0) {
-        const int gb = std::min((n + kSnapThreads - 1) / kSnapThreads, 148 * 8);
+        const int gb = std::min((n + kSnapThreads - 1) / kSnapThreads, 148 * 4);
         snap_extent_kernel<<<gb, kSnapThreads, 0, s>>>(x, y, n, sb.ext);
         snap_project_kernel<<<(n + kSnapThreads - 1) / kSnapThreads, kSnapThreads, 0, s>>>(x, y, label, n, sb.ext,
                                                                                            u, v, counts);
