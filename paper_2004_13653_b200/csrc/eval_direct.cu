@@ -380,52 +380,6 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineArgs a) {
     const int ngxr = gxb - gxa + 1, ng = ngxr * (gyb - gya + 1);
     const int nsub = pg.nsub();
     const int lane = threadIdx.x & 31;
-    if (nsub == 1 && (pg.ww + pg.px - 1) / pg.px + 1 <= 8 && (pg.wh + pg.py - 1) / pg.py + 1 <= 8) {
-        // Direct form (one sub-window per group, <= 8 groups cover a pixel per axis): each
-        // pixel visits only the groups whose window covers it, in the same (gy, gx)
-        // row-major order as the entry list below -- the same sum, bit for bit, without
-        // walking the masked entries.  The tile's slot table is staged in shared memory.
-        int* s_tab = reinterpret_cast<int*>(s_ent);
-        for (int e = threadIdx.x; e < ng; e += blockDim.x) {
-            const int2 gr = a.group[(gya + e / ngxr) * pg.ngx + gxa + e % ngxr];
-            s_tab[e] = gr.y > 0 ? gr.x : -1;
-        }
-        __syncthreads();
-        const int i = X0 + lane;
-        const int gx0 = max(gxa, -floor_div(-(i + F - pg.ww + 1), pg.px)), gx1 = min(gxb, floor_div(i + F, pg.px));
-        const size_t sf = (size_t)pg.slot_floats();
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-            const int j = Y0 + (threadIdx.x >> 5) + 8 * k;
-            const int gy0 = max(gya, -floor_div(-(j + F - pg.wh + 1), pg.py)), gy1 = min(gyb, floor_div(j + F, pg.py));
-            for (int gy = gy0; gy <= gy1; gy++) {
-                const int* row = s_tab + (gy - gya) * ngxr - gxa;
-                const size_t roff = (size_t)(j - (gy * pg.py - F)) * pg.slot_w;
-                float v[8];
-#pragma unroll
-                for (int q = 0; q < 8; q++) {
-                    const int gx = gx0 + q;
-                    v[q] = 0.f;
-                    if (gx <= gx1) {
-                        const int slot = row[gx];
-                        if (slot >= 0) v[q] = a.splat[(size_t)slot * sf + roff + (i - (gx * pg.px - F))];
-                    }
-                }
-#pragma unroll
-                for (int q = 0; q < 8; q++) acc[k] += v[q];
-            }
-        }
-        if (i >= g.W) return;
-        const unsigned long long nf = a.stats[0];
-        const float scale = nf ? (float)(a.c_over_h2 / (double)nf) : 0.f;
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-            const int j = Y0 + (threadIdx.x >> 5) + 8 * k;
-            if (j <= Y1) a.out[(size_t)(j - g.rb) * g.W + i] = acc[k] * scale;
-        }
-        return;
-    }
     if (threadIdx.x < 32) {
         int n = 0;
         for (int gi0 = 0; gi0 < ng; gi0 += 32) {

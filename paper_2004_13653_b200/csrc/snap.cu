@@ -18,7 +18,7 @@
 namespace kde {
 
 constexpr int kSnapThreads = 256;
-constexpr int kRowSeg = 256;    // row pass: outputs per CTA
+constexpr int kRowSeg = 1024;   // row pass: outputs per CTA (4 per thread, 256 apart)
 constexpr int kColW = 32;       // column pass: columns per CTA
 constexpr int kColRows = 64;    // column pass: output rows per CTA
 constexpr int kMaxTaps = 1025;  // 2a + 1 <= 1025 (a <= 512 px)
@@ -146,12 +146,19 @@ __global__ void __launch_bounds__(kSnapThreads) snap_rows_kernel(const uint32_t*
         sr[k] = (xs >= 0 && xs < u) ? (float)row[xs] : 0.f;
     }
     __syncthreads();
-    const int xo = x0 + threadIdx.x;
-    if (xo >= u) return;
-    // tmp(x) = sum_{s=-a..a} k(s) M(x - s): sr[threadIdx.x + a - s] = M(x - s)
-    float acc = 0.f;
-    for (int s = -a; s <= a; s++) acc = fmaf(sw[s + a], sr[threadIdx.x + a - s], acc);
-    tmp[(size_t)y * u + xo] = acc;
+    // tmp(x) = sum_{s=-a..a} k(s) M(x - s): sr[xl + a - s] = M(x - s); each weight read
+    // once for the thread's 4 outputs
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int s = -a; s <= a; s++) {
+        const float w = sw[s + a];
+#pragma unroll
+        for (int q = 0; q < 4; q++) acc[q] = fmaf(w, sr[threadIdx.x + 256 * q + a - s], acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const int xo = x0 + threadIdx.x + 256 * q;
+        if (xo < u) tmp[(size_t)y * u + xo] = acc[q];
+    }
 }
 
 // pass 2: one CTA per (32 columns, 64 rows); the 64 + 2a rows of the 32 columns are
@@ -171,12 +178,19 @@ __global__ void __launch_bounds__(kSnapThreads) snap_cols_kernel(const float* __
     }
     __syncthreads();
     if (xc >= u) return;
-    for (int r = ty; r < kColRows; r += kSnapThreads / 32) {
-        const int yo = y0 + r;
-        if (yo >= v) break;
-        float acc = 0.f;
-        for (int t = -a; t <= a; t++) acc = fmaf(sw[t + a], sc[(r + a - t) * kColW + tx], acc);
-        out[(size_t)yo * u + xc] = acc;
+    constexpr int kR = kColRows / (kSnapThreads / 32);  // 8 output rows per thread
+    float acc[kR];
+#pragma unroll
+    for (int q = 0; q < kR; q++) acc[q] = 0.f;
+    for (int t = -a; t <= a; t++) {  // each weight read once for the thread's 8 outputs
+        const float w = sw[t + a];
+#pragma unroll
+        for (int q = 0; q < kR; q++) acc[q] = fmaf(w, sc[(ty + 8 * q + a - t) * kColW + tx], acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < kR; q++) {
+        const int yo = y0 + ty + 8 * q;
+        if (yo < v) out[(size_t)yo * u + xc] = acc[q];
     }
 }
 
