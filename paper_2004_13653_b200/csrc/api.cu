@@ -261,6 +261,8 @@ int kde_create(const kde_params* p, kde_ctx** out) {
     g.rb = rb;
     g.re = re;
     g.B = choose_bucket(g.R);
+    g.lgB = 0;
+    while ((1 << g.lgB) < g.B) g.lgB++;
     g.F = (int)floor(g.R + 0.5);
     g.nbx = (g.W + g.B - 1) / g.B;
     g.nby = (g.H + g.B - 1) / g.B;

@@ -44,7 +44,7 @@ __device__ __forceinline__ Binned bin_point(double x, double y, const Geom& g, u
     const double fu = floor(u), fv = floor(v);
     const int hx = fu < 0.0 ? 0 : (fu > (double)(g.W - 1) ? g.W - 1 : (int)fu);
     const int hy = fv < 0.0 ? 0 : (fv > (double)(g.H - 1) ? g.H - 1 : (int)fv);
-    const int bx = hx / g.B, by = hy / g.B;
+    const int bx = hx >> g.lgB, by = hy >> g.lgB;  // B is a power of two
     if (by < g.band_lo || by > g.band_hi) return b;  // outside the band's reach
     b.status = 2;
     b.key = (uint32_t)(bx * g.nby + by);  // column-major: a vertical bucket stack is contiguous

@@ -34,7 +34,8 @@ struct Geom {
     double R;             // support half-width in pixels, c_eff * h/res (fp64)
     int W, H;             // raster
     int rb, re;           // band rows [rb, re)
-    int B;                // bucket (point group) edge in pixels
+    int B;                // bucket (point group) edge in pixels (power of two)
+    int lgB;              // log2(B)
     int F;                // floor(R + 1/2): window half-extent beyond the bucket (pixels)
     int nbx, nby;         // bucket grid
     int reach;            // ceil(R + 1/2) + 1 (pixels)
