@@ -261,6 +261,20 @@ def run_ours(args):
         step_e2e(i)
     torch.cuda.synchronize()
     e2e = (time.perf_counter() - t0) * 1e3 / args.steps
+    # context for e2e: the raw pinned host->device copy of the same 16 B/point, alone
+    dx_ = torch.empty_like(xd)
+    dy_ = torch.empty_like(yd)
+    h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dx_.copy_(xh, non_blocking=True)
+    torch.cuda.synchronize()
+    h0.record(stream)
+    for _ in range(5):
+        dx_.copy_(xh, non_blocking=True)
+        dy_.copy_(yh, non_blocking=True)
+    h1.record(stream)
+    torch.cuda.synchronize()
+    h2d_ms = h0.elapsed_time(h1) / 5
+    del dx_, dy_
 
     # --- max over ranks; sum of units over ranks
     useful = st["useful_pairs"]
@@ -323,7 +337,9 @@ def run_ours(args):
         "e2e": {"value": useful / (e2e * 1e-3), "unit": UNIT, "ms_per_step": round(e2e, 4),
                 "h2d_bytes_per_step": 16 * cfg["n"],
                 "d2h_bytes_per_step": 4 * W * H,
-                "note": "pinned host buffers; step i's D2H overlaps step i+1's H2D (pipelined)"},
+                "note": "pinned host buffers; step i's D2H overlaps step i+1's H2D (pipelined)",
+                "h2d_alone_ms": round(h2d_ms, 4),
+                "h2d_alone_gbs": round(16 * cfg["n"] / (h2d_ms * 1e-3) / 1e9, 1)},
         "gpu_launches": int(launches),
         "phases_ms": phases,
         "clocks": clocks,

@@ -65,3 +65,12 @@ def test_dp_full_size_C4_and_errors():
         kde_dp(c.x[:10], c.y[:10], np.array([0, 10], np.int64), -1.0)
     k, nk, r = kde_dp(np.zeros(0), np.zeros(0), np.array([0], np.int64), 1.0)
     assert nk == 0 and r == 0
+
+
+def test_dp_mixed_pointers_rejected():
+    from paper_2004_13653_b200 import KdeError, _lib, kde_dp
+    x = torch.zeros(8, dtype=torch.float64, device="cuda")
+    with pytest.raises(KdeError) as e:
+        kde_dp(x, x, np.array([0, 8], np.int64), 1.0,
+               keep=torch.empty(8, dtype=torch.uint8, device="cuda"))
+    assert e.value.code == _lib.KDE_EINVAL

@@ -108,3 +108,20 @@ def test_snap_full_size_C2_sampled():
     Mp = np.pad(cnt.astype(np.float64), a)
     ref = np.array([w @ Mp[j:j + 2 * a + 1, i:i + 2 * a + 1][::-1, ::-1] @ w for j, i in zip(iy, ix)])
     assert np.abs(out[iy, ix] - ref).max() <= TOL * ref.max()
+
+
+def test_snap_errors():
+    from paper_2004_13653_b200 import KDE, KdeError, _lib
+    x = torch.zeros(4, dtype=torch.float64, device="cuda")
+    k = KDE(0.0, 0.0, 1.0, 32, 32, 2.0, kernel=6 | 0x100)      # radial: not separable
+    with pytest.raises(KdeError) as e:
+        k.snap(x, x)
+    assert e.value.code == _lib.KDE_EUNSUPPORTED
+    k = KDE(0.0, 0.0, 1.0, 32, 32, 2.0, rows=(0, 16))          # banded context
+    with pytest.raises(KdeError) as e:
+        k.snap(x, x)
+    assert e.value.code == _lib.KDE_EUNSUPPORTED
+    k = KDE(0.0, 0.0, 1.0, 32, 32, 2.0)
+    with pytest.raises(KdeError) as e:                          # mixed host / device inputs
+        k.snap(x, torch.zeros(4, dtype=torch.float64))
+    assert e.value.code == _lib.KDE_EINVAL
