@@ -3,7 +3,12 @@
  * estimate of arxiv 2004.13653's visualisation hot path.
  *
  * Citations: P:n = PAPER.md line n (the paper's LaTeX source).
- * §2 restates the operation; DESIGN.md §5 lists the readings (R1..R17).
+ * §2 restates the operation; DESIGN.md §5 lists the readings (R1..R20).
+ *
+ * Entry points: kde_create / kde_load_points / kde_eval / kde_get_stats /
+ * kde_get_bins / kde_set_timing / kde_get_timing / kde_free (the continuous KDE
+ * below, steps a1-a5 of SURVEY.md §8), kde_snap (the paper's own Alg. 3 + Eq. 7
+ * pipeline), kde_dp (GPU Douglas-Peucker), kde_last_error.
  *
  * What it computes (the north star's formula with the paper's Table 1
  * kernels, and Eq. 7's truncated window):

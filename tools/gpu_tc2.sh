@@ -1,0 +1,15 @@
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke $?
+tail -1 gpurun_out/smoke.log
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_snap.py tests/test_gpu_dp.py -x -q -k "tensor or snap_errors or mixed" > gpurun_out/pytest_gpu.log 2>&1; echo pytest $?
+tail -2 gpurun_out/pytest_gpu.log
+rm -f gpurun_out/check.jsonl
+for i in 1 2; do python bench.py --no-cpu-baseline >> gpurun_out/check.jsonl 2>/dev/null; done
+python bench.py --path tensor_split --no-cpu-baseline >> gpurun_out/check.jsonl 2>/dev/null
+python bench.py --config C4 --no-cpu-baseline --steps 10 >> gpurun_out/check.jsonl 2>/dev/null
+python - <<'PY'
+import json
+for l in open("gpurun_out/check.jsonl"):
+    d = json.loads(l)
+    print(d["config"]["config"], d["config"]["path"], d["ms_per_step"], d.get("phases_ms"))
+PY
+echo done
