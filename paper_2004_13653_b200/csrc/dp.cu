@@ -4,13 +4,13 @@
 // removing it) is replaced by level-synchronous rounds over ALL points of ALL
 // trajectories at once.  Every point carries the kept points (s, e) bracketing it -- its
 // current curve segment (the role of the paper's label set Lp, Fig. 5) -- and a round is
-//   dp_ved_kernel     VED (Eq. 9) of every unkept point to its chord, fp64 with
+//   dp_ved16_kernel   VED (Eq. 9) of every unkept point to its chord, fp64 with
 //                     one IEEE rounding per operation in the oracle's order; the
 //                     segment's maximum by atomicMax on the bits (VED >= 0, so the bit
 //                     patterns order like the values) -- the paper's segmented max-scan
-//   dp_argmax_kernel  the earliest index attaining that maximum, when it exceeds eps
+//   dp_argmax16_kernel the earliest index attaining that maximum, when it exceeds eps
 //                     (strict) -- the argmax of the segmented scan
-//   dp_split_kernel   the chosen point becomes a kept point; the others of the segment
+//   dp_split16_kernel the chosen point becomes a kept point; the others of the segment
 //                     move to the half they lie in (the paper's Eq. 11 relabelling)
 // Segments are independent, so processing a whole level at once keeps exactly the point
 // set the recursion keeps (same VED arithmetic, same tie rule).  Rounds run in batches of
@@ -52,64 +52,109 @@ __global__ void dp_init_kernel(const int64_t* __restrict__ offs, int ntraj, int 
     keep[i] = (i == a || i == b) ? 1 : 0;
 }
 
-// keep[i]: 0 active, 1 retained, 2 dropped for good (its segment's maximum VED was <= eps:
-// the segment never splits again, so its points leave the rounds)
-__global__ void dp_ved_kernel(const double* __restrict__ x, const double* __restrict__ y,
-                              const int2* __restrict__ seg, const uint8_t* __restrict__ keep, int n,
-                              unsigned long long* __restrict__ dbits, unsigned long long* __restrict__ best) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int lane = threadIdx.x & 31;
-    const bool act = i < n && keep[i] == 0;
-    int s = -1 - lane;  // unique per inactive lane: never grouped
-    unsigned long long b = 0;
-    if (act) {
+// Working flags: 0 active, 1 retained, 2 retired for good (its segment's maximum VED was
+// <= eps: the segment never splits again, so its points leave the rounds).
+
+// Packed round kernels: one thread per 16 consecutive points (one uint4 of the padded
+// keep flags).  After the first rounds most points are retired, and a thread whose 16
+// flags are all non-zero does nothing but one 16-byte load -- the per-point kernels above
+// pay a CTA launch per 256 points every round instead.
+__device__ __forceinline__ bool any_zero_byte(uint4 v) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t z = 0;
+#pragma unroll
+    for (int q = 0; q < 4; q++) z |= (w[q] - 0x01010101u) & ~w[q] & 0x80808080u;
+    return z != 0;
+}
+__device__ __forceinline__ uint32_t flag_byte(uint4 v, int q) {
+    const uint32_t w = q < 4 ? v.x : q < 8 ? v.y : q < 12 ? v.z : v.w;
+    return (w >> (8 * (q & 3))) & 0xffu;
+}
+
+__global__ void __launch_bounds__(kDpThreads) dp_ved16_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                                                              const int2* __restrict__ seg, const uint4* __restrict__ kp,
+                                                              int nv, unsigned long long* __restrict__ dbits,
+                                                              unsigned long long* __restrict__ best) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nv) return;
+    const uint4 kv = kp[t];
+    if (!any_zero_byte(kv)) return;
+    int cs = -1;                 // current segment run (points of a segment are contiguous)
+    unsigned long long cb = 0;   // its running maximum
+#pragma unroll 4
+    for (int q = 0; q < 16; q++) {
+        if (flag_byte(kv, q) != 0) continue;
+        const int i = 16 * t + q;
         const int2 se = seg[i];
         const double d = dp_ved(x[i], y[i], x[se.x], y[se.x], x[se.y], y[se.y]);
-        b = (unsigned long long)__double_as_longlong(d);
+        const unsigned long long b = (unsigned long long)__double_as_longlong(d);
         dbits[i] = b;
-        s = se.x;
+        if (se.x != cs) {
+            if (cs >= 0) atomicMax(&best[cs], cb);
+            cs = se.x;
+            cb = b;
+        } else if (b > cb) {
+            cb = b;
+        }
     }
-    // lanes of one segment are contiguous: segmented max towards the run's first lane, so
-    // one atomic per (warp, segment) instead of one per point
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long bo = __shfl_down_sync(0xffffffffu, b, o);
-        const int so = __shfl_down_sync(0xffffffffu, s, o);
-        if (lane + o < 32 && so == s) b = bo > b ? bo : b;
-    }
-    const int sp = __shfl_up_sync(0xffffffffu, s, 1);
-    if (act && (lane == 0 || sp != s)) atomicMax(&best[s], b);
+    if (cs >= 0) atomicMax(&best[cs], cb);
 }
 
-__global__ void dp_argmax_kernel(const int2* __restrict__ seg, const uint8_t* __restrict__ keep, int n,
-                                 const unsigned long long* __restrict__ dbits,
-                                 const unsigned long long* __restrict__ best, double eps,
-                                 int* __restrict__ bidx) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n || keep[i] != 0) return;
-    const int s = seg[i].x;
-    const unsigned long long b = best[s];
-    if (dbits[i] == b && __longlong_as_double((long long)b) > eps) atomicMin(&bidx[s], i);
+__global__ void __launch_bounds__(kDpThreads) dp_argmax16_kernel(const int2* __restrict__ seg, const uint4* __restrict__ kp,
+                                                                 int nv, const unsigned long long* __restrict__ dbits,
+                                                                 const unsigned long long* __restrict__ best, double eps,
+                                                                 int* __restrict__ bidx) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nv) return;
+    const uint4 kv = kp[t];
+    if (!any_zero_byte(kv)) return;
+    int done = -1;  // segment whose earliest maximum this thread already reported
+    for (int q = 0; q < 16; q++) {
+        if (flag_byte(kv, q) != 0) continue;
+        const int i = 16 * t + q;
+        const int s = seg[i].x;
+        if (s == done) continue;
+        const unsigned long long b = best[s];
+        if (dbits[i] == b && __longlong_as_double((long long)b) > eps) {
+            atomicMin(&bidx[s], i);
+            done = s;
+        }
+    }
 }
 
-__global__ void dp_split_kernel(int2* __restrict__ seg, uint8_t* __restrict__ keep, int n,
-                                const int* __restrict__ bidx, int* __restrict__ changed) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n || keep[i] != 0) return;
-    const int2 se = seg[i];
-    const int k = bidx[se.x];
-    if (k == kNoSplit) {  // max VED <= eps: the segment is final
-        keep[i] = 2;
-        return;
+__global__ void __launch_bounds__(kDpThreads) dp_split16_kernel(int2* __restrict__ seg, uint4* __restrict__ kp, int nv,
+                                                                const int* __restrict__ bidx, int* __restrict__ changed) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nv) return;
+    const uint4 kv = kp[t];
+    if (!any_zero_byte(kv)) return;
+    uint32_t w[4] = {kv.x, kv.y, kv.z, kv.w};
+    bool any_kept = false;
+    for (int q = 0; q < 16; q++) {
+        if (((w[q >> 2] >> (8 * (q & 3))) & 0xffu) != 0) continue;
+        const int i = 16 * t + q;
+        const int2 se = seg[i];
+        const int k = bidx[se.x];
+        uint32_t nb = 0;
+        if (k == kNoSplit) {  // max VED <= eps: the segment is final
+            nb = 2;
+        } else if (i == k) {
+            nb = 1;
+            any_kept = true;
+        } else if (i > k) {
+            seg[i] = make_int2(k, se.y);
+        } else {
+            seg[i] = make_int2(se.x, k);
+        }
+        w[q >> 2] |= nb << (8 * (q & 3));
     }
-    if (i == k) {
-        keep[i] = 1;
-        *changed = 1;
-    } else if (i > k) {
-        seg[i] = make_int2(k, se.y);
-    } else {
-        seg[i] = make_int2(se.x, k);
-    }
+    kp[t] = make_uint4(w[0], w[1], w[2], w[3]);
+    if (any_kept) *changed = 1;
+}
+
+__global__ void dp_export_kernel(const uint8_t* __restrict__ kp, int n, uint8_t* __restrict__ keep) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;  // 2 (retired) -> 0
+    if (i < n) keep[i] = kp[i] == 1 ? 1 : 0;
 }
 
 __global__ void dp_count_kernel(const uint8_t* __restrict__ keep, int n, unsigned long long* __restrict__ cnt) {
@@ -120,18 +165,26 @@ __global__ void dp_count_kernel(const uint8_t* __restrict__ keep, int n, unsigne
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt, c);
 }
 
-__global__ void dp_finish_kernel(uint8_t* __restrict__ keep, int n) {  // 2 -> 0
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n && keep[i] == 2) keep[i] = 0;
-}
-
 int dp_run(const double* x, const double* y, const int64_t* offs, int ntraj, int n, double eps, uint8_t* keep,
            cudaStream_t s, int64_t* n_kept, int64_t* rounds_out) {
     int2* seg = nullptr;
     unsigned long long *dbits = nullptr, *best = nullptr;
     int *bidx = nullptr, *changed = nullptr;
     int* h_changed = nullptr;
+    uint8_t* kp = nullptr;  // padded working flags: 0 active, 1 retained, 2 retired
+    const int nv = (n + 15) / 16;
+    {   // keep the stream-ordered pool's memory between calls (no re-mapping of ~0.5 GB of
+        // scratch on every call)
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        cudaGetLastError();
+    }
     cudaError_t e = cudaMallocAsync(&seg, sizeof(int2) * (size_t)n, s);
+    if (e == cudaSuccess) e = cudaMallocAsync(&kp, 16 * (size_t)nv, s);
     if (e == cudaSuccess) e = cudaMallocAsync(&dbits, sizeof(unsigned long long) * (size_t)n, s);
     if (e == cudaSuccess) e = cudaMallocAsync(&best, sizeof(unsigned long long) * (size_t)n, s);
     if (e == cudaSuccess) e = cudaMallocAsync(&bidx, sizeof(int) * (size_t)n, s);
@@ -145,15 +198,19 @@ int dp_run(const double* x, const double* y, const int64_t* offs, int ntraj, int
         rc = KDE_ENOMEM;
     } else {
         const int gb = (n + kDpThreads - 1) / kDpThreads;
-        dp_init_kernel<<<gb, kDpThreads, 0, s>>>(offs, ntraj, n, seg, keep);
+        const int gv = (nv + kDpThreads - 1) / kDpThreads;
+        cudaMemsetAsync(kp, 1, 16 * (size_t)nv, s);  // padding: retained (never active)
+        dp_init_kernel<<<gb, kDpThreads, 0, s>>>(offs, ntraj, n, seg, kp);
         for (;;) {
             cudaMemsetAsync(changed, 0, sizeof(int) * kDpBatch, s);
             for (int r = 0; r < kDpBatch; r++) {
                 cudaMemsetAsync(best, 0, sizeof(unsigned long long) * (size_t)n, s);
                 cudaMemsetAsync(bidx, 0x7f, sizeof(int) * (size_t)n, s);  // kNoSplit
-                dp_ved_kernel<<<gb, kDpThreads, 0, s>>>(x, y, seg, keep, n, dbits, best);
-                dp_argmax_kernel<<<gb, kDpThreads, 0, s>>>(seg, keep, n, dbits, best, eps, bidx);
-                dp_split_kernel<<<gb, kDpThreads, 0, s>>>(seg, keep, n, bidx, changed + r);
+                const uint4* kp4 = reinterpret_cast<const uint4*>(kp);
+                dp_ved16_kernel<<<gv, kDpThreads, 0, s>>>(x, y, seg, kp4, nv, dbits, best);
+                dp_argmax16_kernel<<<gv, kDpThreads, 0, s>>>(seg, kp4, nv, dbits, best, eps, bidx);
+                dp_split16_kernel<<<gv, kDpThreads, 0, s>>>(seg, reinterpret_cast<uint4*>(kp), nv, bidx,
+                                                            changed + r);
             }
             cudaMemcpyAsync(h_changed, changed, sizeof(int) * kDpBatch, cudaMemcpyDeviceToHost, s);
             e = cudaStreamSynchronize(s);
@@ -168,7 +225,7 @@ int dp_run(const double* x, const double* y, const int64_t* offs, int ntraj, int
             if (last < kDpBatch - 1) break;  // a round changed nothing: converged
         }
     }
-    if (rc == KDE_OK) dp_finish_kernel<<<(n + kDpThreads - 1) / kDpThreads, kDpThreads, 0, s>>>(keep, n);
+    if (rc == KDE_OK) dp_export_kernel<<<(n + kDpThreads - 1) / kDpThreads, kDpThreads, 0, s>>>(kp, n, keep);
     if (rc == KDE_OK && n_kept) {  // the kept count, read back once
         unsigned long long* d_cnt = dbits;  // scratch reuse
         cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), s);
@@ -183,6 +240,7 @@ int dp_run(const double* x, const double* y, const int64_t* offs, int ntraj, int
     }
     if (rounds_out) *rounds_out = rounds;
     cudaFreeAsync(seg, s);
+    cudaFreeAsync(kp, s);
     cudaFreeAsync(dbits, s);
     cudaFreeAsync(best, s);
     cudaFreeAsync(bidx, s);
