@@ -292,10 +292,25 @@ def run_ours(args):
 
     peaks, peak_src = _peaks()
     clocks = clk.summary()
-    if path == "direct":
+    clk = peaks.get("sm_max_mhz", 1965.0) * 1e6
+    if path == "direct" and cfg["radial"]:
+        # radial forms evaluate K per pair: Gaussian / Triangular /
+        # Tricube need one MUFU op per pair (ex2 or sqrt: XU pipe, 16/clk/SM), Cosine two
+        # (sqrt + cos: 8/clk/SM); the polynomial ones ~4 FMA-pipe ops (s^2+t^2, clamp, poly)
+        kname = cfg["kernel"]
+        if kname in ("gaussian", "triangular", "tricube", "cosine"):
+            per_clk = 8 if kname == "cosine" else 16
+            bound, src = "xu", f"derived: 148 SMs x {per_clk} MUFU pair-evals/clk x sm_max_mhz"
+        else:
+            per_clk, bound, src = 32, "alu", "derived: 148 SMs x 128 FP32 ops/clk / 4 ops per pair x sm_max_mhz"
+        peak = 148 * per_clk * clk / 1e9
+        roof = {"bound": bound, "kernel": "splat_kernel",
+                "achieved": st["useful_pairs"] / (eval_ms * 1e-3) / 1e9,
+                "peak": round(peak, 1), "unit": "Gevals/s", "peak_source": f"{src} ({peak_src})"}
+    elif path == "direct":
         # ALU-bound: 1 FFMA (2 flops) per useful pair; FP32 peak = 148 SMs x 128 FFMA/clk
         # x 2 flops x max SM clock
-        peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        peak = 148 * 128 * 2 * clk / 1e12
         roof = {"bound": "alu", "kernel": "splat_kernel",
                 "achieved": 2.0 * st["useful_pairs"] / (eval_ms * 1e-3) / 1e12,
                 "peak": round(peak, 2), "unit": "TFLOP/s",

@@ -24,7 +24,9 @@ namespace kde {
 
 constexpr int kDpThreads = 256;
 constexpr int kDpBatch = 4;
-constexpr int kNoSplit = 0x7f7f7f7f;  // bidx after the per-round memset of 0x7f bytes (> any index)
+constexpr int kNoSplit = 0x7f7f7f7f;
+constexpr int kLocalMax = 1024;     // trajectories up to this length: one CTA, shared memory
+constexpr int kLocalThreads = 256;  // bidx after the per-round memset of 0x7f bytes (> any index)
 
 // Eq. 9: |P_sP_n x P_sP_e| / |P_sP_e|; a degenerate chord uses |P_n - P_s| (R14)
 __device__ __forceinline__ double dp_ved(double px, double py, double sx, double sy, double ex, double ey) {
@@ -49,7 +51,74 @@ __global__ void dp_init_kernel(const int64_t* __restrict__ offs, int ntraj, int 
     }
     const int a = (int)offs[lo], b = (int)offs[lo + 1] - 1;
     seg[i] = make_int2(a, b);
-    keep[i] = (i == a || i == b) ? 1 : 0;
+    // trajectories of <= kLocalMax points are finished by dp_local_kernel: inactive here
+    keep[i] = (i == a || i == b || b - a + 1 <= kLocalMax) ? 1 : 0;
+}
+
+// A whole trajectory of <= kLocalMax points per CTA, every round in shared memory (the same
+// VED arithmetic and tie rule as the global rounds, so the same kept set): no global
+// traffic per round, only CTA barriers.  Writes keep[] for its trajectory.
+__global__ void __launch_bounds__(kLocalThreads) dp_local_kernel(const double* __restrict__ x,
+                                                                 const double* __restrict__ y,
+                                                                 const int64_t* __restrict__ offs, double eps,
+                                                                 uint8_t* __restrict__ keep) {
+    __shared__ double sx[kLocalMax], sy[kLocalMax];
+    __shared__ unsigned long long sb[kLocalMax];  // per segment start: max VED bits
+    __shared__ int si[kLocalMax];                  // per segment start: earliest argmax
+    __shared__ short2 sg[kLocalMax];               // per point: its segment (start, end)
+    __shared__ uint8_t fl[kLocalMax];              // 0 active, 1 kept, 2 retired
+    __shared__ int s_changed;
+    const int a = (int)offs[blockIdx.x], L = (int)offs[blockIdx.x + 1] - a;
+    if (L > kLocalMax || L <= 0) return;
+    const int tid = threadIdx.x;
+    for (int i = tid; i < L; i += kLocalThreads) {
+        sx[i] = x[a + i];
+        sy[i] = y[a + i];
+        fl[i] = (i == 0 || i == L - 1) ? 1 : 0;
+        sg[i] = make_short2(0, (short)(L - 1));
+        sb[i] = 0ull;
+        si[i] = 0x7fffffff;
+    }
+    __syncthreads();
+    for (;;) {
+        if (tid == 0) s_changed = 0;
+        for (int i = tid; i < L; i += kLocalThreads) {  // VED, segment maxima
+            if (fl[i] != 0) continue;
+            const short2 se = sg[i];
+            const double d = dp_ved(sx[i], sy[i], sx[se.x], sy[se.x], sx[se.y], sy[se.y]);
+            atomicMax(&sb[se.x], (unsigned long long)__double_as_longlong(d));
+        }
+        __syncthreads();
+        for (int i = tid; i < L; i += kLocalThreads) {  // earliest argmax above eps
+            if (fl[i] != 0) continue;
+            const short2 se = sg[i];
+            const double d = dp_ved(sx[i], sy[i], sx[se.x], sy[se.x], sx[se.y], sy[se.y]);
+            const unsigned long long b = sb[se.x];
+            if ((unsigned long long)__double_as_longlong(d) == b && __longlong_as_double((long long)b) > eps)
+                atomicMin(&si[se.x], i);
+        }
+        __syncthreads();
+        for (int i = tid; i < L; i += kLocalThreads) {  // split / retire
+            if (fl[i] != 0) continue;
+            const short2 se = sg[i];
+            const int k = si[se.x];
+            if (k == 0x7fffffff) fl[i] = 2;
+            else if (i == k) {
+                fl[i] = 1;
+                s_changed = 1;
+            } else if (i > k) sg[i] = make_short2((short)k, se.y);
+            else sg[i] = make_short2(se.x, (short)k);
+        }
+        __syncthreads();
+        const int changed = s_changed;
+        for (int i = tid; i < L; i += kLocalThreads) {
+            sb[i] = 0ull;
+            si[i] = 0x7fffffff;
+        }
+        __syncthreads();
+        if (!changed) break;
+    }
+    for (int i = tid; i < L; i += kLocalThreads) keep[a + i] = fl[i] == 1 ? 1 : 0;
 }
 
 // Working flags: 0 active, 1 retained, 2 retired for good (its segment's maximum VED was
@@ -225,7 +294,10 @@ int dp_run(const double* x, const double* y, const int64_t* offs, int ntraj, int
             if (last < kDpBatch - 1) break;  // a round changed nothing: converged
         }
     }
-    if (rc == KDE_OK) dp_export_kernel<<<(n + kDpThreads - 1) / kDpThreads, kDpThreads, 0, s>>>(kp, n, keep);
+    if (rc == KDE_OK) {
+        dp_export_kernel<<<(n + kDpThreads - 1) / kDpThreads, kDpThreads, 0, s>>>(kp, n, keep);
+        if (ntraj > 0) dp_local_kernel<<<ntraj, kLocalThreads, 0, s>>>(x, y, offs, eps, keep);
+    }
     if (rc == KDE_OK && n_kept) {  // the kept count, read back once
         unsigned long long* d_cnt = dbits;  // scratch reuse
         cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), s);

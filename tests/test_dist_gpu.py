@@ -30,3 +30,20 @@ def test_two_rank_row_bands_bitwise(tmp_path):
     assert r.returncode == 0, r.stderr[-3000:]
     v = json.loads(out.read_text())
     assert v["direct"] and v["tensor"], v
+
+
+def test_bench_two_ranks_prints_one_line():
+    """bench.py's N > 1 path (row bands + all-gather, max over ranks) end to end; gloo when
+    the box has one GPU (both ranks share it)."""
+    backend = "nccl" if torch.cuda.device_count() >= 2 else "gloo"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", "C1", "--steps", "3",
+           "--warmup", "3", "--no-cpu-baseline", "--dist-backend", backend]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["parallelism"] == "row-bands x2"
+    assert d["useful_pairs"] > 0 and d["roofline"]["frac"] > 0
