@@ -252,7 +252,8 @@ KDE_API int kde_snap(kde_ctx* c, const double* x, const double* y, const int32_t
  * computes the VED (Eq. 9, fp64, one rounding per operation) of every
  * unretained point to its current chord, keeps the earliest point of maximal VED of every
  * segment whose maximum is strictly larger than eps, and splits the segment there;
- * it stops when a round keeps nothing.  The kept set equals the serial recursion's
+ * it stops when a round keeps nothing (trajectories of <= 4096 points run all their
+ * rounds inside one CTA in shared memory).  The kept set equals the serial recursion's
  * (R14: strict >, earliest index on ties, degenerate chord -> point distance).
  *   x, y          [in]  n fp64 coordinates (n = traj_offsets[ntraj]), all trajectories
  *                       concatenated (the paper's merged store, TLen)
@@ -261,7 +262,8 @@ KDE_API int kde_snap(kde_ctx* c, const double* x, const double* y, const int32_t
  *   eps           [in]  threshold, finite, >= 0 (same units as x, y)
  *   keep          [out] n uint8: 1 = retained (end points always)
  *   device        [in]  CUDA ordinal; stream [in] cudaStream_t
- *   n_kept, rounds [out] NULL or host int64: retained count, rounds run
+ *   n_kept, rounds [out] NULL or host int64: retained count, and the number of
+ *                 levels that retained a point (the recursion depth)
  * Pointers: all device (on `device`) or all host (staged through the device).
  * Synchronous (one 4-byte readback per 4 rounds).  Errors: KDE_EINVAL, KDE_ENOMEM, KDE_ECUDA.
  */

@@ -25,8 +25,8 @@ namespace kde {
 constexpr int kDpThreads = 256;
 constexpr int kDpBatch = 4;
 constexpr int kNoSplit = 0x7f7f7f7f;
-constexpr int kLocalMax = 1024;     // trajectories up to this length: one CTA, shared memory
-constexpr int kLocalThreads = 256;  // bidx after the per-round memset of 0x7f bytes (> any index)
+constexpr int kLocalMax = 4096;     // trajectories up to this length: one CTA, shared memory
+constexpr size_t local_smem(int lmax) { return (size_t)lmax * (8 + 8 + 8 + 4 + 4 + 1); }  // bidx after the per-round memset of 0x7f bytes (> any index)
 
 // Eq. 9: |P_sP_n x P_sP_e| / |P_sP_e|; a degenerate chord uses |P_n - P_s| (R14)
 __device__ __forceinline__ double dp_ved(double px, double py, double sx, double sy, double ex, double ey) {
@@ -58,18 +58,21 @@ __global__ void dp_init_kernel(const int64_t* __restrict__ offs, int ntraj, int 
 // A whole trajectory of <= kLocalMax points per CTA, every round in shared memory (the same
 // VED arithmetic and tie rule as the global rounds, so the same kept set): no global
 // traffic per round, only CTA barriers.  Writes keep[] for its trajectory.
-__global__ void __launch_bounds__(kLocalThreads) dp_local_kernel(const double* __restrict__ x,
-                                                                 const double* __restrict__ y,
-                                                                 const int64_t* __restrict__ offs, double eps,
-                                                                 uint8_t* __restrict__ keep) {
-    __shared__ double sx[kLocalMax], sy[kLocalMax];
-    __shared__ unsigned long long sb[kLocalMax];  // per segment start: max VED bits
-    __shared__ int si[kLocalMax];                  // per segment start: earliest argmax
-    __shared__ short2 sg[kLocalMax];               // per point: its segment (start, end)
-    __shared__ uint8_t fl[kLocalMax];              // 0 active, 1 kept, 2 retired
+template <int LMIN, int LMAX, int T>
+__global__ void __launch_bounds__(T) dp_local_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                                                     const int64_t* __restrict__ offs, double eps,
+                                                     uint8_t* __restrict__ keep, int* __restrict__ rounds) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    double* sx = reinterpret_cast<double*>(dsm);                       // [LMAX]
+    double* sy = sx + LMAX;                                             // [LMAX]
+    unsigned long long* sb = reinterpret_cast<unsigned long long*>(sy + LMAX);  // per segment start: max VED bits
+    int* si = reinterpret_cast<int*>(sb + LMAX);                        // per segment start: earliest argmax
+    short2* sg = reinterpret_cast<short2*>(si + LMAX);                  // per point: its segment (start, end)
+    uint8_t* fl = reinterpret_cast<uint8_t*>(sg + LMAX);                // 0 active, 1 kept, 2 retired
     __shared__ int s_changed;
+    constexpr int kLocalThreads = T;
     const int a = (int)offs[blockIdx.x], L = (int)offs[blockIdx.x + 1] - a;
-    if (L > kLocalMax || L <= 0) return;
+    if (L > LMAX || L < LMIN || L <= 0) return;
     const int tid = threadIdx.x;
     for (int i = tid; i < L; i += kLocalThreads) {
         sx[i] = x[a + i];
@@ -80,7 +83,9 @@ __global__ void __launch_bounds__(kLocalThreads) dp_local_kernel(const double* _
         si[i] = 0x7fffffff;
     }
     __syncthreads();
+    int nround = 0;
     for (;;) {
+        nround++;
         if (tid == 0) s_changed = 0;
         for (int i = tid; i < L; i += kLocalThreads) {  // VED, segment maxima
             if (fl[i] != 0) continue;
@@ -119,6 +124,7 @@ __global__ void __launch_bounds__(kLocalThreads) dp_local_kernel(const double* _
         if (!changed) break;
     }
     for (int i = tid; i < L; i += kLocalThreads) keep[a + i] = fl[i] == 1 ? 1 : 0;
+    if (tid == 0) atomicMax(rounds, nround - 1);  // the last round kept nothing
 }
 
 // Working flags: 0 active, 1 retained, 2 retired for good (its segment's maximum VED was
@@ -296,7 +302,26 @@ int dp_run(const double* x, const double* y, const int64_t* offs, int ntraj, int
     }
     if (rc == KDE_OK) {
         dp_export_kernel<<<(n + kDpThreads - 1) / kDpThreads, kDpThreads, 0, s>>>(kp, n, keep);
-        if (ntraj > 0) dp_local_kernel<<<ntraj, kLocalThreads, 0, s>>>(x, y, offs, eps, keep);
+        if (ntraj > 0) {  // short trajectories: 256 threads, 6 CTAs/SM; long: 1024 threads
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(dp_local_kernel<0, 1024, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)local_smem(1024));
+                cudaFuncSetAttribute(dp_local_kernel<1025, kLocalMax, 1024>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)local_smem(kLocalMax));
+                attr = true;
+            }
+            int* d_lr = changed;  // scratch reuse: the local kernels' deepest round count
+            cudaMemsetAsync(d_lr, 0, sizeof(int), s);
+            dp_local_kernel<0, 1024, 256><<<ntraj, 256, local_smem(1024), s>>>(x, y, offs, eps, keep, d_lr);
+            dp_local_kernel<1025, kLocalMax, 1024><<<ntraj, 1024, local_smem(kLocalMax), s>>>(x, y, offs, eps,
+                                                                                              keep, d_lr);
+            int lr = 0;
+            e = cudaMemcpyAsync(&lr, d_lr, sizeof(int), cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+            if (e != cudaSuccess) rc = cuda_fail(e, "kde_dp: local rounds");
+            rounds = std::max<int64_t>(rounds, lr);
+        }
     }
     if (rc == KDE_OK && n_kept) {  // the kept count, read back once
         unsigned long long* d_cnt = dbits;  // scratch reuse
