@@ -39,7 +39,7 @@ template <int H> struct TcShape {
     static constexpr int kChunk = 32 * H;
     static constexpr int kABytes = kTcM * kChunk * 2;
     static constexpr int kSBO = 512 * H;
-    static constexpr int kMinBlocks = H == 1 ? 8 : 5;  // CTAs per SM (smem, TMEM, registers)
+    static constexpr int kMinBlocks = H == 1 ? 7 : 5;  // CTAs per SM (smem, TMEM, registers)
 };
 
 struct TcArgs {
