@@ -32,5 +32,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2_snap.csv python bench.py --path snap --steps 5 --warmup 3 > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:tc_splat_kernel -c 1 -o gpurun_out/c2_tensor -f python bench.py --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"^splat_kernel|segreduce|combine|rs_downsweep|bin_convert|gather_kernel" -c 8 -o gpurun_out/c2_direct -f python bench.py --path direct --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_dp.csv python tools/dp_prof.py > /dev/null 2>&1
 ls gpurun_out
 echo done
