@@ -1,8 +1,14 @@
 #!/usr/bin/env python
 """Benchmark of the gridded-KDE hot path.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--path auto|direct|tensor]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--dp-eps E]
+                    [--path auto|direct|tensor|tensor_split|snap]
     python bench.py --impl reference ...      # the fp64 CPU oracle on the host cores
+
+Default workload: C4, the config BASELINE.json's metric is quoted on (Zhoushan-Islands-
+shaped 20M raw points, 8192^2, Gaussian h = 4 px, cutoff 4h); --dp-eps 0.5|1|5 evaluates
+the same trajectories Douglas-Peucker-compressed by the library's kde_dp (PAPER.md
+Table 4 thresholds).  `--gpus N` outside torchrun spawns N ranks itself.
 
 A step is one pass of the whole hot path over one batch of synthetic input that is
 already resident in HBM: kde_load_points (a1 convert/keys, a2 stable counting sort +
@@ -62,63 +68,92 @@ def _peaks():
                 "sm_max_mhz": 1965.0}, "fallback"
 
 
-def _traffic(kernel_name):
-    """dram bytes/launch of the dominant kernel from the committed ncu capture, if any."""
+def _traffic(key):
+    """dram read+write bytes per launch of the dominant kernel, from the committed ncu
+    capture of exactly this workload (profiles/traffic.json, keyed "<config>/<path>/<kernel>"
+    by profiles/summarize.py); None when no capture of this workload exists."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            return json.load(f).get(kernel_name)
+            return json.load(f).get(key)
     except Exception:
         return None
 
 
-class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+def _workload_key(args):
+    """The traffic/profile key of this run: config (+ bandwidth, kernel, form, DP eps)."""
+    cfg = args.cfg
+    k = args.config
+    if args.hpx is not None:
+        k += f"-h{cfg['hpx']:g}"
+    if args.kernel is not None:
+        k += f"-{cfg['kernel']}"
+    if cfg["radial"]:
+        k += "-radial"
+    if args.dp_eps is not None:
+        k += f"-dp{args.dp_eps:g}"
+    return k
 
-    def __init__(self, dev):
+
+class ClockSampler:
+    """SM clocks + throttle reasons sampled through NVML every ~2 ms during the timed
+    region (nvidia-smi's 50 ms floor gave only a couple of samples per region)."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, dev, period=0.002):
         self.dev = dev
+        self.period = period
         self.rows = []
-        self.proc = None
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.t = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self._nvml_index())
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self.t = threading.Thread(target=self._poll, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.t = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 6:
-                self.rows.append(parts)
+    def _nvml_index(self):
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            ids = [v.strip() for v in vis.split(",") if v.strip()]
+            if self.dev < len(ids) and ids[self.dev].isdigit():
+                return int(ids[self.dev])
+        return self.dev
+
+    def _poll(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                self.rows.append((sm, rs))
+            except Exception:
+                pass
+            time.sleep(self.period)
 
     def __exit__(self, *a):
-        if self.proc:
-            time.sleep(0.12)
-            self.proc.terminate()
-            try:
-                self.proc.wait(2)
-            except Exception:
-                self.proc.kill()
+        if self.t is not None:
+            time.sleep(self.period)
+            self._stop.set()
+            self.t.join(1.0)
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[2 + k] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({k for _, rs in self.rows for k, bit in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_min_mhz": min(sm), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.rows), "source": "nvml, 2 ms period"}
 
 
 def _dist():
@@ -128,10 +163,37 @@ def _dist():
     return ws, rank, local
 
 
-def _gen(cfg):
+class _Cloud:
+    def __init__(self, x, y, traj_offsets):
+        self.x, self.y, self.traj_offsets = x, y, traj_offsets
+
+
+def _gen(cfg, dp_eps=None, device=None):
+    """The config's seeded synthetic input; with dp_eps, the same trajectories compressed by
+    the library's own GPU Douglas-Peucker (kde_dp) at that threshold (in
+    metres) -- input preparation, outside every timed region."""
     import aisgen
     cloud = aisgen.generate(cfg["preset"], cfg["n"], aisgen.SEED_BASE + cfg["idx"])
     x0, y0, res = aisgen.grid_for(cfg["preset"], cfg["W"])
+    if dp_eps is not None and device == "oracle":
+        # reference arm (CPU): the serial oracle DP, which the GPU kde_dp matches bit for bit
+        import oracle
+        keep = oracle.dp_compress(cloud.x, cloud.y, cloud.traj_offsets, float(dp_eps)).astype(bool)
+        kc = np.concatenate([[0], np.cumsum(keep.astype(np.int64))])
+        cloud = _Cloud(cloud.x[keep], cloud.y[keep], kc[np.asarray(cloud.traj_offsets, np.int64)])
+    elif dp_eps is not None:
+        import torch
+
+        from paper_2004_13653_b200 import kde_dp
+        dev = device if device is not None else torch.device("cuda", 0)
+        offs = np.asarray(cloud.traj_offsets, np.int64)
+        xd, yd, od = (torch.from_numpy(a).to(dev) for a in (cloud.x, cloud.y, offs))
+        keep, nk, _ = kde_dp(xd, yd, od, float(dp_eps), device=dev.index or 0)
+        keep = keep.bool()
+        x, y = xd[keep].cpu().numpy(), yd[keep].cpu().numpy()
+        kc = np.concatenate([[0], np.cumsum(keep.cpu().numpy().astype(np.int64))])
+        cloud = _Cloud(x, y, kc[offs])
+        assert len(x) == nk
     return cloud, x0, y0, res
 
 
@@ -152,7 +214,8 @@ def run_ours(args):
             dist.init_process_group(args.dist_backend)
     cfg = args.cfg
     W = H = cfg["W"]
-    cloud, x0, y0, res = _gen(cfg)
+    cloud, x0, y0, res = _gen(cfg, args.dp_eps, dev)
+    n_pts = len(cloud.x)
     from paper_2004_13653_b200.dist import assemble, plan_bands
     bands = plan_bands(H, ws, 256)
     rows = bands[rank] if ws > 1 else (0, H)
@@ -316,21 +379,27 @@ def run_ours(args):
                 "peak": round(peak, 2), "unit": "TFLOP/s",
                 "peak_source": "derived: 148 SMs x 128 FP32 FMA/clk x 2 x sm_max_mhz (%s)" % peak_src}
     else:
-        # tensor-pipe bound: the contraction's executed MMA flops
-        # (kde_stats.tc_mma_flops: 2 x 128 x N x 16 x 2 per 32-point chunk) per kernel time,
-        # against the fp16 dense peak; the useful-pair share of those flops next to it
-        peak = peaks["bf16_tflops"]  # fp16 dense = bf16 dense rate (guide's nominal ratio 1)
+        # tensor-pipe bound.  achieved = the METHOD's work: 2 flops per
+        # useful (pixel, point) pair per kernel time, against the dense fp16 peak (fp16 dense
+        # = bf16 dense rate, the guide's nominal ratio 1).  The executed MMA flops
+        # (kde_stats.tc_mma_flops: chunks x 2 x 128 x N x 16 x 2, zero padding included) and
+        # their tensor-pipe share are reported beside it.
+        peak = peaks["bf16_tflops"]
         mma = st["tc_mma_flops"] * (3 if path == "tensor_split" else 1)  # split: 3 MMAs / K step
+        useful_tf = 2.0 * st["useful_pairs"] / (eval_ms * 1e-3) / 1e12
         roof = {"bound": "tensor", "kernel": "tc_splat_kernel",
-                "achieved": mma / (eval_ms * 1e-3) / 1e12,
+                "achieved": useful_tf,
                 "peak": peak, "unit": "TFLOP/s",
                 "peak_source": f"{peak_src} bf16_tflops (fp16 dense rate = bf16)",
-                "mma_flops_per_launch": mma,
-                "useful_tflops": round(2.0 * st["useful_pairs"] / (eval_ms * 1e-3) / 1e12, 3),
+                "achieved_counts": "2 flops per useful pair (kde_stats.useful_pairs)",
+                "executed_mma_flops_per_launch": mma,
+                "executed_mma_tflops": round(mma / (eval_ms * 1e-3) / 1e12, 3),
+                "executed_frac": round(mma / (eval_ms * 1e-3) / 1e12 / peak, 4),
                 "useful_share_of_mma": round(2.0 * st["useful_pairs"] / max(mma, 1), 4)}
     roof["achieved"] = round(roof["achieved"], 3)
     roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
-    roof["traffic"] = _traffic(roof["kernel"])
+    roof["traffic"] = _traffic(f"{_workload_key(args)}/{path}/{roof['kernel']}")
+    roof["traffic_key"] = f"{_workload_key(args)}/{path}/{roof['kernel']}"
     roof["kernel_ms"] = round(eval_ms, 4)
 
     line = {
@@ -340,8 +409,11 @@ def run_ours(args):
         "vs_baseline": None, "dtype": {"direct": "f32", "tensor": "f16xf16->f32",
                                         "tensor_split": "(f16+f16)x(f16+f16)->f32"}[path],
         "data": "synthetic (aisgen, seeded)",
-        "config": {"workload": WORKLOAD[args.config], "config": args.config, "path": path,
-                   "n_points": cfg["n"], "grid": f"{W}x{H}", "h_px": cfg["hpx"],
+        "config": {"workload": _workload_name(args, n_pts), "config": args.config, "path": path,
+                   "n_points": n_pts, "grid": f"{W}x{H}", "h_px": cfg["hpx"],
+                   "dp_eps_m": args.dp_eps,
+                   "dp_compression_pct": (round(100.0 * (1 - n_pts / cfg["n"]), 2)
+                                          if args.dp_eps is not None else None),
                    "cutoff": cfg["cutoff"], "kernel": cfg["kernel"],
                    "form": "radial" if cfg["radial"] else "product",
                    "parallelism": f"row-bands x{ws}" if ws > 1 else "single",
@@ -350,11 +422,11 @@ def run_ours(args):
         "useful_pairs": useful,
         "step_ms_rank0": step_stats,
         "e2e": {"value": useful / (e2e * 1e-3), "unit": UNIT, "ms_per_step": round(e2e, 4),
-                "h2d_bytes_per_step": 16 * cfg["n"],
+                "h2d_bytes_per_step": 16 * n_pts,
                 "d2h_bytes_per_step": 4 * W * H,
                 "note": "pinned host buffers; step i's D2H overlaps step i+1's H2D (pipelined)",
                 "h2d_alone_ms": round(h2d_ms, 4),
-                "h2d_alone_gbs": round(16 * cfg["n"] / (h2d_ms * 1e-3) / 1e9, 1)},
+                "h2d_alone_gbs": round(16 * n_pts / (h2d_ms * 1e-3) / 1e9, 1)},
         "gpu_launches": int(launches),
         "phases_ms": phases,
         "clocks": clocks,
@@ -365,6 +437,15 @@ def run_ours(args):
     if ws > 1:
         dist.destroy_process_group()
     print(json.dumps(line), flush=True)
+
+
+def _workload_name(args, n_pts):
+    w = WORKLOAD[args.config]
+    if args.hpx is not None:
+        w += f" at h={args.cfg['hpx']:g}px"
+    if args.dp_eps is not None:
+        w += f", Douglas-Peucker-compressed at eps={args.dp_eps:g} m ({n_pts} points kept)"
+    return w
 
 
 def run_snap(args):
@@ -495,7 +576,7 @@ def run_reference(args):
     if rank != 0:
         return  # rank 0 alone runs the CPU oracle
     cfg = args.cfg
-    cloud, x0, y0, res = _gen(cfg)
+    cloud, x0, y0, res = _gen(cfg, args.dp_eps, "oracle")
     per = max(2.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
     import oracle
     oracle.build()
@@ -510,8 +591,9 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (aisgen, seeded)",
-        "config": {"workload": WORKLOAD[args.config], "config": args.config,
-                   "n_points": cfg["n"], "grid": f"{W}x{W}", "h_px": cfg["hpx"],
+        "config": {"workload": _workload_name(args, len(cloud.x)), "config": args.config,
+                   "n_points": len(cloud.x), "grid": f"{W}x{W}", "h_px": cfg["hpx"],
+                   "dp_eps_m": args.dp_eps,
                    "cutoff": cfg["cutoff"], "kernel": cfg["kernel"],
                    "form": "radial" if cfg["radial"] else "product", "parallelism": "host threads"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": vals[0]["cores"], "kind": "oracle",
@@ -521,21 +603,41 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def _spawn(args):
+    """`bench.py --gpus N` outside torchrun: launch N ranks of this script on this node
+    (one process per GPU, rendezvous on 127.0.0.1), rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2", choices=list(CONFIGS))
+    # C4 (Zhoushan-shaped 20M points, 8192^2, Gaussian h = 4 px) is the config BASELINE's
+    # metric is quoted on
+    ap.add_argument("--config", default="C4", choices=list(CONFIGS))
     ap.add_argument("--path", default="auto", choices=["auto", "direct", "tensor", "tensor_split", "snap"])
     ap.add_argument("--kernel", default=None, help="Table-1 kernel name (default: the config's)")
     ap.add_argument("--radial", action="store_true", help="radial form K(||.||/h) (DESIGN.md R1)")
     ap.add_argument("--hpx", type=float, default=None, help="bandwidth in pixels (C5 sweep)")
+    ap.add_argument("--dp-eps", type=float, default=None,
+                    help="Douglas-Peucker threshold in metres: evaluate the DP-compressed input "
+                         "(C4: 0.5, 1.0, 5.0 -- PAPER.md Table 4 thresholds)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_spawn(args))
     args.warmup = max(args.warmup, 3)
     cfg = dict(CONFIGS[args.config])
     if args.kernel is not None:

@@ -265,7 +265,11 @@ KDE_API int kde_snap(kde_ctx* c, const double* x, const double* y, const int32_t
  *   n_kept, rounds [out] NULL or host int64: retained count, and the number of
  *                 levels that retained a point (the recursion depth)
  * Pointers: all device (on `device`) or all host (staged through the device).
- * Synchronous (one 4-byte readback per 4 rounds).  Errors: KDE_EINVAL, KDE_ENOMEM, KDE_ECUDA.
+ * Synchronous (one 4-byte readback per 4 rounds).  Errors: KDE_EINVAL (traj_offsets[0] != 0,
+ * decreasing offsets, n out of range, pointers on another device), KDE_ENOMEM, KDE_ECUDA.
+ * The offsets are validated on the host (device offsets are copied back once).  A point
+ * with a non-finite coordinate has a NaN VED, which -- as in the serial recursion's
+ * `d > dmax` -- never becomes a segment maximum.
  */
 KDE_API int kde_dp(const double* x, const double* y, const int64_t* traj_offsets, int64_t ntraj, double eps,
                    uint8_t* keep, int32_t device, void* stream, int64_t* n_kept, int64_t* rounds);

@@ -112,10 +112,31 @@ def _ptr(a):
     return a.data_ptr()
 
 
+# ctx handle -> (band rows, raster rows H, width, device): the sizes the C calls write into
+# caller buffers, so the binding can check them (the ABI takes plain pointers)
+_SHAPES: dict = {}
+
+
 def kde_create(params: kde_params) -> int:
     h = ctypes.c_void_p()
     _check(_L.kde_create(ctypes.byref(params), ctypes.byref(h)))
+    rb, re = int(params.row_begin), int(params.row_end)
+    if rb == 0 and re == 0:
+        re = int(params.height)
+    _SHAPES[h.value] = (re - rb, int(params.height), int(params.width), int(params.device))
     return h.value
+
+
+def _check_out(ctx, t, numel, what, dtypes=("torch.float32",)):
+    if str(t.dtype) not in dtypes or not getattr(t, "is_cuda", False):
+        raise TypeError(f"{what} must be a CUDA tensor of dtype {' or '.join(dtypes)}")
+    if not t.is_contiguous():
+        raise ValueError(f"{what} must be contiguous")
+    shp = _SHAPES.get(ctx)
+    if shp is not None and t.device.index != shp[3]:
+        raise ValueError(f"{what} is on cuda:{t.device.index}, the context on cuda:{shp[3]}")
+    if t.numel() < numel:
+        raise ValueError(f"{what} holds {t.numel()} elements, needs {numel}")
 
 
 def kde_load_points(ctx: int, x, y) -> None:
@@ -133,8 +154,8 @@ def kde_load_points(ctx: int, x, y) -> None:
 
 def kde_eval(ctx: int, path: int, out, stream: int | None = None) -> None:
     """out: float32 CUDA tensor of band_rows*W; stream: raw cudaStream_t handle."""
-    if str(out.dtype) != "torch.float32" or not out.is_cuda:
-        raise TypeError("out must be a float32 CUDA tensor")
+    shp = _SHAPES.get(ctx)
+    _check_out(ctx, out, shp[0] * shp[2] if shp else 0, "out")
     if stream is None:
         import torch
         stream = torch.cuda.current_stream(out.device).cuda_stream
@@ -148,8 +169,11 @@ def kde_snap(ctx: int, x, y, label, out, counts=None, stream: int | None = None)
     n = int(x.shape[0])
     if int(y.shape[0]) != n or (label is not None and int(label.shape[0]) != n):
         raise ValueError("x, y and label lengths differ")
-    if str(out.dtype) != "torch.float32" or not out.is_cuda:
-        raise TypeError("out must be a float32 CUDA tensor")
+    shp = _SHAPES.get(ctx)
+    npx = shp[1] * shp[2] if shp else 0
+    _check_out(ctx, out, npx, "out")
+    if counts is not None:
+        _check_out(ctx, counts, npx, "counts", ("torch.int32", "torch.uint32"))
     if label is not None and str(label.dtype) not in ("int32", "torch.int32"):
         raise TypeError("labels must be int32")
     if stream is None:
@@ -167,6 +191,21 @@ def kde_dp(x, y, traj_offsets, eps: float, keep=None, device: int = 0, stream: i
     n = int(x.shape[0])
     ntraj = int(traj_offsets.shape[0]) - 1
     dev = not isinstance(x, np.ndarray) and x.is_cuda
+    # the C call reads n from traj_offsets[ntraj]: check the offsets against the buffers
+    # (a mismatch would index x, y, keep out of bounds)
+    if ntraj < 0:
+        raise ValueError("traj_offsets must hold at least one entry")
+    offs = traj_offsets.cpu().numpy() if hasattr(traj_offsets, "cpu") else np.asarray(traj_offsets)
+    if str(offs.dtype) != "int64":
+        raise TypeError("traj_offsets must be int64")
+    if offs[0] != 0 or np.any(np.diff(offs) < 0) or int(offs[-1]) != n or int(y.shape[0]) != n:
+        raise ValueError("traj_offsets must start at 0, be nondecreasing and end at len(x) == len(y)")
+    if keep is not None and int(keep.shape[0]) < n:
+        raise ValueError("keep is shorter than x")
+    for a in (y, traj_offsets) + ((keep,) if keep is not None else ()):
+        adev = not isinstance(a, np.ndarray) and a.is_cuda
+        if adev != dev or (dev and a.device != x.device):
+            raise ValueError("x, y, traj_offsets and keep must all be on the same device (or host)")
     if keep is None:
         if dev:
             import torch
@@ -215,4 +254,5 @@ def kde_get_timing(ctx: int) -> dict:
 
 def kde_free(ctx: int | None) -> None:
     if ctx:
+        _SHAPES.pop(ctx, None)
         _L.kde_free(ctx)

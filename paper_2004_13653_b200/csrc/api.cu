@@ -512,7 +512,10 @@ int kde_get_stats(const kde_ctx* c, kde_stats* s) {
     const EvalPlan& tp = c->plan[KDE_PATH_TENSOR];
     if (c->loaded && tp.enabled && tp.planned_gen == c->load_gen) {  // executed MMA flops / eval
         int chunks = 0;
-        const cudaError_t e = cudaMemcpy(&chunks, tp.d_totals + kTotChunks, sizeof(int), cudaMemcpyDeviceToHost);
+        // the plan was built on the eval's (possibly non-blocking) stream: wait for that
+        // eval before reading its totals
+        cudaError_t e = c->evaluated ? cudaEventSynchronize(c->evald_ev) : cudaSuccess;
+        if (e == cudaSuccess) e = cudaMemcpy(&chunks, tp.d_totals + kTotChunks, sizeof(int), cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) return cuda_fail(e, "kde_get_stats");
         // per chunk: chunk_pts/16 MMAs of M=128 x N x K=16, 2 flops per MAC
         s->tc_mma_flops = (int64_t)chunks * (tp.pg.chunk_pts / 16) * 2 * kTcM * tp.pg.mma_n * 16;
@@ -635,14 +638,28 @@ int kde_dp(const double* x, const double* y, const int64_t* traj_offsets, int64_
     cudaStream_t s = (cudaStream_t)stream;
     int dd = -1;
     const bool dev = is_device_ptr(traj_offsets, &dd);
-    int64_t n = 0;
+    // the offsets decide every index the kernels touch: validate them on the host
+    // (offsets[0] == 0, nondecreasing; n = offsets[ntraj]) -- device offsets are copied back
+    // once (8 B per trajectory)
+    std::vector<int64_t> ho((size_t)ntraj + 1);
     if (dev) {
-        if (cudaMemcpyAsync(&n, traj_offsets + ntraj, sizeof n, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        if (cudaMemcpyAsync(ho.data(), traj_offsets, sizeof(int64_t) * (ntraj + 1), cudaMemcpyDeviceToHost, s) !=
+                cudaSuccess ||
             cudaStreamSynchronize(s) != cudaSuccess)
             return cuda_fail(cudaGetLastError(), "kde_dp: offsets readback");
     } else {
-        n = traj_offsets[ntraj];
+        memcpy(ho.data(), traj_offsets, sizeof(int64_t) * (ntraj + 1));
     }
+    if (ho[0] != 0) {
+        set_error("kde_dp: traj_offsets[0] = %lld (must be 0)", (long long)ho[0]);
+        return KDE_EINVAL;
+    }
+    for (int64_t t = 0; t < ntraj; t++)
+        if (ho[t + 1] < ho[t]) {
+            set_error("kde_dp: traj_offsets decrease at %lld", (long long)t);
+            return KDE_EINVAL;
+        }
+    const int64_t n = ho[ntraj];
     if (n < 0 || n > 2147483647ll - 4096) {
         set_error("kde_dp: %lld points outside [0, 2^31 - 4097]", (long long)n);
         return KDE_EINVAL;
@@ -657,6 +674,10 @@ int kde_dp(const double* x, const double* y, const int64_t* traj_offsets, int64_
     int d1 = -1, d2 = -1, d3 = -1;
     if (is_device_ptr(x, &d1) != dev || is_device_ptr(y, &d2) != dev || is_device_ptr(keep, &d3) != dev) {
         set_error("kde_dp: x, y, traj_offsets and keep must all be host or all device pointers");
+        return KDE_EINVAL;
+    }
+    if (dev && (d1 != device || d2 != device || d3 != device || dd != device)) {
+        set_error("kde_dp: device pointers must be on device %d", device);
         return KDE_EINVAL;
     }
     if (dev) return dp_run(x, y, traj_offsets, (int)ntraj, (int)n, eps, keep, s, n_kept, rounds);

@@ -440,14 +440,13 @@ int bin_points(kde_ctx* c, const double* d_x, const double* d_y, int64_t n64) {
         const bool staged = nbins <= env_staged;
         const size_t dn_smem =
             sizeof(uint32_t) * (2 * nbins + (staged ? 2 * tile : 0)) + sizeof(uint16_t) * 8 * nbins;
-        static bool attr = false;
-        if (!attr) {  // largest case: 1024 digits, tile 4096, staged
+        {   // the shared-memory opt-in is per device and cheap: set it on every load (no
+            // process-global state).  Largest case: 1024 digits, tile 4096, staged.
             const int mx = (int)(sizeof(uint32_t) * (2 * 1024 + 2 * 4096) + sizeof(uint16_t) * 8 * 1024);
             cudaFuncSetAttribute(rs_downsweep<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
             cudaFuncSetAttribute(rs_downsweep<true, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
             cudaFuncSetAttribute(rs_downsweep<false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
             cudaFuncSetAttribute(rs_downsweep<false, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-            attr = true;
         }
         bin_convert_kernel<<<nblk, kRsThreads, up_smem, s>>>(d_x, d_y, n, g, nb, pb.key[0], pb.rec,
                                                              c->d_stats, dmask, pb.hist, nblk, rounds);

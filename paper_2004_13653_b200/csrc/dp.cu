@@ -38,6 +38,14 @@ __device__ __forceinline__ double dp_ved(double px, double py, double sx, double
     return __ddiv_rn(fabs(cr), L);
 }
 
+// The bits a VED takes part in the segment maximum with.  The serial recursion keeps a
+// point only if `d > dmax` (dp_oracle.c), so a NaN VED (a non-finite coordinate) never
+// becomes the maximum: NaN maps to the bits of 0.0, which never exceeds eps >= 0 and never
+// equals a positive maximum -- the kept set stays the recursion's.
+__device__ __forceinline__ unsigned long long ved_bits(double d) {
+    return isnan(d) ? 0ull : (unsigned long long)__double_as_longlong(d);
+}
+
 // segment of every point: its trajectory's end points; end points are kept
 __global__ void dp_init_kernel(const int64_t* __restrict__ offs, int ntraj, int n, int2* __restrict__ seg,
                                uint8_t* __restrict__ keep) {
@@ -91,7 +99,7 @@ __global__ void __launch_bounds__(T) dp_local_kernel(const double* __restrict__ 
             if (fl[i] != 0) continue;
             const short2 se = sg[i];
             const double d = dp_ved(sx[i], sy[i], sx[se.x], sy[se.x], sx[se.y], sy[se.y]);
-            atomicMax(&sb[se.x], (unsigned long long)__double_as_longlong(d));
+            atomicMax(&sb[se.x], ved_bits(d));
         }
         __syncthreads();
         for (int i = tid; i < L; i += kLocalThreads) {  // earliest argmax above eps
@@ -99,7 +107,7 @@ __global__ void __launch_bounds__(T) dp_local_kernel(const double* __restrict__ 
             const short2 se = sg[i];
             const double d = dp_ved(sx[i], sy[i], sx[se.x], sy[se.x], sx[se.y], sy[se.y]);
             const unsigned long long b = sb[se.x];
-            if ((unsigned long long)__double_as_longlong(d) == b && __longlong_as_double((long long)b) > eps)
+            if (ved_bits(d) == b && __longlong_as_double((long long)b) > eps)
                 atomicMin(&si[se.x], i);
         }
         __syncthreads();
@@ -162,7 +170,7 @@ __global__ void __launch_bounds__(kDpThreads) dp_ved16_kernel(const double* __re
         const int i = 16 * t + q;
         const int2 se = seg[i];
         const double d = dp_ved(x[i], y[i], x[se.x], y[se.x], x[se.y], y[se.y]);
-        const unsigned long long b = (unsigned long long)__double_as_longlong(d);
+        const unsigned long long b = ved_bits(d);
         dbits[i] = b;
         if (se.x != cs) {
             if (cs >= 0) atomicMax(&best[cs], cb);
@@ -293,6 +301,11 @@ int dp_run(const double* x, const double* y, const int64_t* offs, int ntraj, int
                 rc = cuda_fail(e, "kde_dp");
                 break;
             }
+            e = cudaGetLastError();  // the round kernels' launches
+            if (e != cudaSuccess) {
+                rc = cuda_fail(e, "kde_dp: round launch");
+                break;
+            }
             int last = -1;
             for (int r = 0; r < kDpBatch; r++)
                 if (h_changed[r]) last = r;
@@ -303,21 +316,26 @@ int dp_run(const double* x, const double* y, const int64_t* offs, int ntraj, int
     if (rc == KDE_OK) {
         dp_export_kernel<<<(n + kDpThreads - 1) / kDpThreads, kDpThreads, 0, s>>>(kp, n, keep);
         if (ntraj > 0) {  // short trajectories: 256 threads, 6 CTAs/SM; long: 1024 threads
-            static bool attr = false;
-            if (!attr) {
-                cudaFuncSetAttribute(dp_local_kernel<0, 1024, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            // the shared-memory opt-in is per device: set it on every call (cheap), and
+            // check both launches (a failed launch must not leave the pre-marked keep flags)
+            e = cudaFuncSetAttribute(dp_local_kernel<0, 1024, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)local_smem(1024));
-                cudaFuncSetAttribute(dp_local_kernel<1025, kLocalMax, 1024>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)local_smem(kLocalMax));
-                attr = true;
-            }
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(dp_local_kernel<1025, kLocalMax, 1024>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)local_smem(kLocalMax));
             int* d_lr = changed;  // scratch reuse: the local kernels' deepest round count
-            cudaMemsetAsync(d_lr, 0, sizeof(int), s);
-            dp_local_kernel<0, 1024, 256><<<ntraj, 256, local_smem(1024), s>>>(x, y, offs, eps, keep, d_lr);
-            dp_local_kernel<1025, kLocalMax, 1024><<<ntraj, 1024, local_smem(kLocalMax), s>>>(x, y, offs, eps,
-                                                                                              keep, d_lr);
+            if (e == cudaSuccess) e = cudaMemsetAsync(d_lr, 0, sizeof(int), s);
+            if (e == cudaSuccess) {
+                dp_local_kernel<0, 1024, 256><<<ntraj, 256, local_smem(1024), s>>>(x, y, offs, eps, keep, d_lr);
+                e = cudaGetLastError();
+            }
+            if (e == cudaSuccess) {
+                dp_local_kernel<1025, kLocalMax, 1024><<<ntraj, 1024, local_smem(kLocalMax), s>>>(x, y, offs, eps,
+                                                                                                  keep, d_lr);
+                e = cudaGetLastError();
+            }
             int lr = 0;
-            e = cudaMemcpyAsync(&lr, d_lr, sizeof(int), cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(&lr, d_lr, sizeof(int), cudaMemcpyDeviceToHost, s);
             if (e == cudaSuccess) e = cudaStreamSynchronize(s);
             if (e != cudaSuccess) rc = cuda_fail(e, "kde_dp: local rounds");
             rounds = std::max<int64_t>(rounds, lr);

@@ -93,6 +93,8 @@ struct SnapBufs {
     float* tmp = nullptr;            // Eq. 7 row pass
     unsigned long long* ext = nullptr;  // encoded x/y extent
     float* w = nullptr;              // 1-D weights
+    cudaEvent_t done = nullptr;      // end of the last kde_snap: the next one (on any stream)
+    bool used = false;               // waits for it before rewriting the scratch above
 };
 
 struct EvalPlan {

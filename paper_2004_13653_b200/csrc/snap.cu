@@ -203,6 +203,7 @@ void snap_free(kde_ctx* c) {
     cudaFree(sb.tmp);
     cudaFree(sb.ext);
     cudaFree(sb.w);
+    if (sb.done) cudaEventDestroy(sb.done);
     sb = SnapBufs();
 }
 
@@ -248,6 +249,17 @@ int snap_run(kde_ctx* c, const double* x, const double* y, const int32_t* label,
     if (2 * a + 1 > kMaxTaps) {
         set_error("kde_snap: window 2a+1 = %d exceeds %d taps", 2 * a + 1, kMaxTaps);
         return KDE_EUNSUPPORTED;
+    }
+    if (!sb.done && cudaEventCreateWithFlags(&sb.done, cudaEventDisableTiming) != cudaSuccess)
+        return cuda_fail(cudaGetLastError(), "kde_snap: event");
+    // the scratch below (staging, extent, weights, M_D, row pass) is per context: a snap on
+    // another stream must not overwrite it while the previous one still reads it
+    if (sb.used) {
+        if (host) {
+            const cudaError_t we = cudaEventSynchronize(sb.done);  // its buffers are reallocated/overwritten
+            if (we != cudaSuccess) return cuda_fail(we, "kde_snap: previous call");
+        }
+        cudaStreamWaitEvent(s, sb.done, 0);
     }
     if (host && n > sb.cap) {
         if (grow_snap((void**)&sb.x, sizeof(double) * n, "x") || grow_snap((void**)&sb.y, sizeof(double) * n, "y") ||
@@ -296,6 +308,8 @@ int snap_run(kde_ctx* c, const double* x, const double* y, const int32_t* label,
     c->launches += 2;
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "kde_snap launch");
+    cudaEventRecord(sb.done, s);
+    sb.used = true;
     if (host) {  // the caller's host buffers must outlive the copies
         const cudaError_t se = cudaStreamSynchronize(s);
         if (se != cudaSuccess) return cuda_fail(se, "kde_snap");

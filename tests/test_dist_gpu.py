@@ -47,3 +47,17 @@ def test_bench_two_ranks_prints_one_line():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["parallelism"] == "row-bands x2"
     assert d["useful_pairs"] > 0 and d["roofline"]["frac"] > 0
+
+
+def test_bench_gpus_flag_spawns_ranks_itself():
+    """`bench.py --gpus 2` without torchrun launches its own 2 ranks (rank 0 prints)."""
+    backend = "nccl" if torch.cuda.device_count() >= 2 else "gloo"
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", "C1",
+           "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--dist-backend", backend]
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "row-bands x2"

@@ -67,10 +67,53 @@ def test_dp_full_size_C4_and_errors():
     assert nk == 0 and r == 0
 
 
+def _raw_dp(x, y, offs, keep, eps=1.0):
+    """The C ABI call itself (no binding-side checks)."""
+    import ctypes
+
+    from paper_2004_13653_b200 import _lib
+    nk, r = ctypes.c_int64(0), ctypes.c_int64(0)
+    return _lib._L.kde_dp(_lib._ptr(x), _lib._ptr(y), _lib._ptr(offs), int(offs.shape[0]) - 1, float(eps),
+                          _lib._ptr(keep), 0, None, ctypes.byref(nk), ctypes.byref(r))
+
+
 def test_dp_mixed_pointers_rejected():
-    from paper_2004_13653_b200 import KdeError, _lib, kde_dp
+    from paper_2004_13653_b200 import _lib, kde_dp
     x = torch.zeros(8, dtype=torch.float64, device="cuda")
-    with pytest.raises(KdeError) as e:
-        kde_dp(x, x, np.array([0, 8], np.int64), 1.0,
-               keep=torch.empty(8, dtype=torch.uint8, device="cuda"))
-    assert e.value.code == _lib.KDE_EINVAL
+    keep = torch.empty(8, dtype=torch.uint8, device="cuda")
+    with pytest.raises(ValueError):  # the binding checks devices first
+        kde_dp(x, x, np.array([0, 8], np.int64), 1.0, keep=keep)
+    assert _raw_dp(x, x, np.array([0, 8], np.int64), keep) == _lib.KDE_EINVAL  # and so does the C ABI
+
+
+def test_dp_bad_offsets_rejected():
+    """offsets not starting at 0, decreasing, or not matching the buffers."""
+    from paper_2004_13653_b200 import _lib, kde_dp
+    x = np.zeros(8)
+    keep = np.zeros(8, np.uint8)
+    for offs in ([1, 8], [0, 5, 3, 8], [0, 9]):
+        with pytest.raises(ValueError):
+            kde_dp(x, x, np.array(offs, np.int64), 1.0, keep=keep)
+    for offs in ([1, 8], [0, 5, 3, 8]):  # host offsets through the raw C call
+        assert _raw_dp(x, x, np.array(offs, np.int64), keep) == _lib.KDE_EINVAL
+    xd = torch.zeros(8, dtype=torch.float64, device="cuda")
+    kd = torch.empty(8, dtype=torch.uint8, device="cuda")
+    od = torch.tensor([0, 6, 2, 8], dtype=torch.int64, device="cuda")  # device offsets, decreasing
+    assert _raw_dp(xd, xd, od, kd) == _lib.KDE_EINVAL
+
+
+def test_dp_nan_points_match_serial_recursion():
+    """a non-finite coordinate gives a NaN VED, which the recursion's `d > dmax`
+    never selects; the GPU maps it below every finite VED (bit-exact kept set)."""
+    c = aisgen.generate("islands", 200_000, 33)
+    x, y = c.x.copy(), c.y.copy()
+    rng = np.random.default_rng(4)
+    idx = rng.choice(len(x), 300, replace=False)
+    x[idx[:150]] = np.nan
+    y[idx[150:250]] = np.inf
+    x[idx[250:]] = -np.inf
+    for eps in (0.0, 1.0, 5.0):
+        ref = oracle.dp_compress(x, y, c.traj_offsets, eps)
+        keep, nk, _ = _gpu(x, y, c.traj_offsets, eps)
+        np.testing.assert_array_equal(keep, ref)
+        assert nk == int(ref.sum())

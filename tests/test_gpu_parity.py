@@ -185,6 +185,11 @@ def test_error_paths_on_device():
     with pytest.raises(KdeError) as e:
         k.eval("tensor")
     assert e.value.code == _lib.KDE_EUNSUPPORTED
+    # the binding checks the caller's raster buffer (the ABI takes a plain pointer)
+    with pytest.raises(ValueError):
+        k.eval("direct", out=torch.empty(c["W"] * c["H"] - 1, dtype=torch.float32, device="cuda"))
+    with pytest.raises(TypeError):
+        k.eval("direct", out=torch.empty(c["W"] * c["H"], dtype=torch.float64, device="cuda"))
 
 
 # --- tensor-core Gaussian path (a4): 2e-3 * max -----------------------------------------
