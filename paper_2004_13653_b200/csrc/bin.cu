@@ -66,10 +66,15 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
 // ---------------------------------------------------------------------------------
 // a2 constants (the convert kernel below already works in sort tiles)
 constexpr int kRsThreads = 256;
-constexpr int kRsMaxBits = 10;
-// A sort tile is kRsThreads x rounds keys, rounds = max(8, nbins / 64): tiles hold at least
-// 4 keys per digit, so the per-tile histograms stay <= 1/4 of the keys.
-inline int rs_rounds(int nbins) { return nbins / 64 > 8 ? nbins / 64 : 8; }
+constexpr int kRsMaxBits = 11;
+// A sort tile is kRsThreads x rounds keys, rounds = max(8, nbins / 64) rounded up to a
+// power of two: tiles hold at least 4 keys per digit, so the per-tile histograms stay <= 1/4
+// of the keys.
+inline int rs_rounds(int nbins) {
+    int r = 8;
+    while (r * 64 + 64 < nbins) r *= 2;  // (a last digit set of 2^k + 1 keeps 2^k / 64)
+    return r;
+}
 
 // a1 kernel, one sort tile (kRsThreads x rounds points) per CTA: keys, the point's record (bucket-
 // local fp32 coordinates + packed int16 ranges, read back by the gather), the integer
@@ -78,9 +83,8 @@ inline int rs_rounds(int nbins) { return nbins / 64 > 8 ? nbins / 64 : 8; }
 __global__ void __launch_bounds__(kRsThreads, 4) bin_convert_kernel(
     const double* __restrict__ x, const double* __restrict__ y, int n, Geom g, uint32_t sentinel,
     uint32_t* __restrict__ key, uint4* __restrict__ rec, unsigned long long* __restrict__ stats,
-    uint32_t dmask, uint32_t* __restrict__ hist, int nblk, int rounds) {
-    extern __shared__ uint32_t h[];  // [dmask + 1]
-    const int nbins = (int)dmask + 1;
+    uint32_t dmask, int nbins, uint32_t* __restrict__ hist, int hstride, int rounds) {
+    extern __shared__ uint32_t h[];  // [nbins]
     for (int d = threadIdx.x; d < nbins; d += kRsThreads) h[d] = 0;
     unsigned long long nf = 0, no = 0, up = 0;
     const int rb = g.rb, re = g.re;
@@ -129,7 +133,7 @@ __global__ void __launch_bounds__(kRsThreads, 4) bin_convert_kernel(
         for (int k = 0; k < kRsThreads / 32; k++) t += s[threadIdx.x][k];
         if (t) atomicAdd(&stats[threadIdx.x], t);
     }
-    for (int d = threadIdx.x; d < nbins; d += kRsThreads) hist[(size_t)d * nblk + blockIdx.x] = h[d];
+    for (int d = threadIdx.x; d < nbins; d += kRsThreads) hist[(size_t)d * hstride + blockIdx.x] = h[d];
 }
 
 // ---------------------------------------------------------------------------------
@@ -141,10 +145,9 @@ __global__ void __launch_bounds__(kRsThreads, 4) bin_convert_kernel(
 // -> coalesced write-out, each tile adding the exclusive scan of the digit totals.
 
 __global__ void __launch_bounds__(kRsThreads) rs_upsweep(const uint32_t* __restrict__ keys, int n,
-                                                         int shift, uint32_t dmask,
-                                                         uint32_t* __restrict__ hist, int nblk, int rounds) {
-    extern __shared__ uint32_t h[];  // [dmask + 1]
-    const int nbins = (int)dmask + 1;
+                                                         int shift, uint32_t dmask, int nbins,
+                                                         uint32_t* __restrict__ hist, int hstride, int rounds) {
+    extern __shared__ uint32_t h[];  // [nbins]
     for (int d = threadIdx.x; d < nbins; d += kRsThreads) h[d] = 0;
     __syncthreads();
     const int base = blockIdx.x * kRsThreads * rounds;
@@ -154,7 +157,7 @@ __global__ void __launch_bounds__(kRsThreads) rs_upsweep(const uint32_t* __restr
         if (i < n) atomicAdd(&h[(keys[i] >> shift) & dmask], 1u);
     }
     __syncthreads();
-    for (int d = threadIdx.x; d < nbins; d += kRsThreads) hist[(size_t)d * nblk + blockIdx.x] = h[d];
+    for (int d = threadIdx.x; d < nbins; d += kRsThreads) hist[(size_t)d * hstride + blockIdx.x] = h[d];
 }
 
 // exclusive scan of a[0..nb) in shared memory, in place (all kRsThreads threads call it)
@@ -203,12 +206,11 @@ __device__ __forceinline__ void block_scan_smem(uint32_t* a, int nb, uint32_t* s
 template <bool STAGED, int ROUNDS>
 __global__ void __launch_bounds__(kRsThreads) rs_downsweep(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
-    uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, int n, int shift, uint32_t dmask,
-    const uint32_t* __restrict__ hscan, const uint32_t* __restrict__ dtot, int nblk) {
+    uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, int n, int shift, uint32_t dmask, int nbins,
+    const uint32_t* __restrict__ hscan, const uint32_t* __restrict__ dtot, int hstride) {
     extern __shared__ uint32_t sm[];
     __shared__ uint32_t s_ws[kRsThreads / 32];
     constexpr int kW = kRsThreads / 32;
-    const int nbins = (int)dmask + 1;
     constexpr int tile = kRsThreads * ROUNDS;
     uint32_t* boff = sm;                    // [nbins] global base of the tile's digit run
     uint32_t* dstart = sm + nbins;          // [nbins] tile-local start of the digit run
@@ -257,7 +259,7 @@ __global__ void __launch_bounds__(kRsThreads) rs_downsweep(
     __syncthreads();
     block_scan_smem(boff, nbins, s_ws);
     if (STAGED) block_scan_smem(dstart, nbins, s_ws);
-    for (int d = t; d < nbins; d += kRsThreads) boff[d] += hscan[(size_t)d * nblk + b];  // + tile prefix
+    for (int d = t; d < nbins; d += kRsThreads) boff[d] += hscan[(size_t)d * hstride + b];  // + tile prefix
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < ROUNDS; r++) {
@@ -287,94 +289,113 @@ __global__ void __launch_bounds__(kRsThreads) rs_downsweep(
     }
 }
 
-// Per-digit exclusive scan over the tiles, in place (hist is digit-major [d][tile]), one
-// CTA per digit (each thread a run of consecutive tiles); dtot[d] = the digit's total.
-__global__ void __launch_bounds__(256) rs_scan_digits(uint32_t* __restrict__ hist, int nbins, int nblk,
-                                                      uint32_t* __restrict__ dtot) {
+// Per-digit exclusive scan over the tiles, in place (hist is digit-major [d][stride], rows
+// 16-byte aligned), one CTA per digit: coalesced uint4 loads of 1024 tiles per step, a block
+// scan, a running carry; dtot[d] = the digit's total.
+__global__ void __launch_bounds__(256) rs_scan_digits(uint32_t* __restrict__ hist, int nbins, int ntiles,
+                                                      int stride, uint32_t* __restrict__ dtot) {
     __shared__ uint32_t s_ws[8];
     const int d = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    uint32_t* row = hist + (size_t)d * nblk;
-    const int per = (nblk + 255) / 256;
-    const int b0 = t * per, b1 = min(b0 + per, nblk);
-    uint32_t sum = 0;
-    for (int b = b0; b < b1; b++) sum += row[b];
-    uint32_t inc = sum;
+    uint32_t* row = hist + (size_t)d * stride;
+    uint32_t carry = 0;
+    for (int base = 0; base < ntiles; base += 1024) {
+        const int i = base + 4 * t;
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (i + 3 < ntiles) {
+            v = *reinterpret_cast<const uint4*>(row + i);
+        } else {
+            if (i < ntiles) v.x = row[i];
+            if (i + 1 < ntiles) v.y = row[i + 1];
+            if (i + 2 < ntiles) v.z = row[i + 2];
+        }
+        const uint32_t sum = v.x + v.y + v.z + v.w;
+        uint32_t inc = sum;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += u;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
+        }
+        if (lane == 31) s_ws[warp] = inc;
+        __syncthreads();
+        uint32_t pre = 0, tot = 0;
+#pragma unroll
+        for (int w = 0; w < 8; w++) {
+            const uint32_t x = s_ws[w];
+            pre += w < warp ? x : 0u;
+            tot += x;
+        }
+        __syncthreads();  // s_ws is rewritten by the next step
+        uint4 o;
+        o.x = carry + pre + inc - sum;
+        o.y = o.x + v.x;
+        o.z = o.y + v.y;
+        o.w = o.z + v.z;
+        if (i + 3 < ntiles) {
+            *reinterpret_cast<uint4*>(row + i) = o;
+        } else {
+            if (i < ntiles) row[i] = o.x;
+            if (i + 1 < ntiles) row[i + 1] = o.y;
+            if (i + 2 < ntiles) row[i + 2] = o.z;
+        }
+        carry += tot;
     }
-    if (lane == 31) s_ws[warp] = inc;
-    __syncthreads();
-    uint32_t pre = inc - sum, tot = 0;
-    for (int w = 0; w < 8; w++) {
-        if (w < warp) pre += s_ws[w];
-        tot += s_ws[w];
-    }
-    for (int b = b0; b < b1; b++) {
-        const uint32_t v = row[b];
-        row[b] = pre;
-        pre += v;
-    }
-    if (t == 0) dtot[d] = tot;
+    if (t == 0) dtot[d] = carry;
 }
 
-// bucket offsets from the sorted keys: offsets[b] = first position with key >= b.  The
-// thread of position d writes the buckets (key[d-1], key[d]] (empty buckets take the next
-// occupied bucket's start); long runs of empty buckets are written by the whole warp.
-__global__ void offsets_kernel(const uint32_t* __restrict__ skey, int n, uint32_t nb,
-                               uint32_t* __restrict__ offsets) {
+// a2 gather + bucket offsets, one pass over the sorted keys.  Position d in [0, n]:
+//   offsets: offsets[b] = first position with key >= b -- the thread of position d writes the
+//            buckets (key[d-1], key[d]] (empty buckets take the next occupied bucket's start;
+//            long runs of empty buckets are written by the whole warp);
+//   gather:  a kept point (key < nb) at sorted position d gets its bucket-local fp32 SoA and
+//            packed int16 ranges from the record the convert kernel wrote in input order.
+// Kept keys (< nb) sort before the dropped sentinel nb, so positions [0, n_binned) are the
+// binned points.
+__global__ void __launch_bounds__(256) gather_offsets_kernel(const uint4* __restrict__ rec,
+                                                             const uint32_t* __restrict__ perm,
+                                                             const uint32_t* __restrict__ skey, int n, uint32_t nb,
+                                                             uint32_t* __restrict__ offsets,
+                                                             float2* __restrict__ xy, uint2* __restrict__ rng) {
     const int lane = threadIdx.x & 31;
-    const int stride = gridDim.x * blockDim.x;
-    for (int d0 = blockIdx.x * blockDim.x; d0 <= n; d0 += stride) {  // warp-uniform trip count
-        const int d = d0 + (threadIdx.x & ~31) + lane;
-        int64_t lo = 0, hi = -1;  // buckets [lo, hi] take position d
-        if (d <= n) {
-            lo = (d > 0 ? (int64_t)skey[d - 1] : -1) + 1;
-            hi = d < n ? (int64_t)min(skey[d], nb) : (int64_t)nb;
-        }
-        const bool big = hi - lo >= 8;
-        if (!big)
-            for (int64_t b = lo; b <= hi; b++) offsets[b] = (uint32_t)d;
-        uint32_t m = __ballot_sync(0xffffffffu, big);
-        while (m) {
-            const int src = __ffs(m) - 1;
-            m &= m - 1;
-            const int64_t s0 = __shfl_sync(0xffffffffu, lo, src), s1 = __shfl_sync(0xffffffffu, hi, src);
-            const int dv = __shfl_sync(0xffffffffu, d, src);
-            for (int64_t b = s0 + lane; b <= s1; b += 32) offsets[b] = (uint32_t)dv;
-        }
-    }
-}
-
-// a2 gather: sorted position -> bucket-local fp32 SoA + packed int16 ranges, from the
-// records the convert kernel wrote in input order
-__global__ void __launch_bounds__(256) gather_kernel(const uint4* __restrict__ rec,
-                                                     const uint32_t* __restrict__ perm,
-                                                     const uint32_t* __restrict__ offsets, uint32_t nb,
-                                                     float2* __restrict__ xy, uint2* __restrict__ rng) {
-    const int nbin = (int)offsets[nb];
     constexpr int U = 4;
     const int tile = blockDim.x * U;
-    for (int d0 = blockIdx.x * tile + threadIdx.x; d0 < nbin; d0 += gridDim.x * tile) {
-        uint32_t q[U];
+    for (int d0 = blockIdx.x * tile; d0 <= n; d0 += gridDim.x * tile) {  // warp-uniform trip count
+        uint32_t kc[U], kp[U], q[U];
         uint4 r[U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
-            const int d = d0 + u * blockDim.x;
-            q[u] = d < nbin ? perm[d] : 0u;
+            const int d = d0 + u * blockDim.x + (threadIdx.x & ~31) + lane;
+            kc[u] = d < n ? skey[d] : nb;
+            kp[u] = (d > 0 && d <= n) ? skey[d - 1] : 0xffffffffu;
+            q[u] = (d < n && kc[u] < nb) ? perm[d] : 0u;
         }
 #pragma unroll
         for (int u = 0; u < U; u++) {
-            const int d = d0 + u * blockDim.x;
-            r[u] = d < nbin ? rec[q[u]] : make_uint4(0u, 0u, 0u, 0u);
+            const int d = d0 + u * blockDim.x + (threadIdx.x & ~31) + lane;
+            r[u] = (d < n && kc[u] < nb) ? rec[q[u]] : make_uint4(0u, 0u, 0u, 0u);
         }
 #pragma unroll
         for (int u = 0; u < U; u++) {
-            const int d = d0 + u * blockDim.x;
-            if (d >= nbin) break;
-            xy[d] = make_float2(__uint_as_float(r[u].x), __uint_as_float(r[u].y));
-            rng[d] = make_uint2(r[u].z, r[u].w);
+            const int d = d0 + u * blockDim.x + (threadIdx.x & ~31) + lane;
+            int64_t lo = 0, hi = -1;  // buckets [lo, hi] take position d
+            if (d <= n) {
+                lo = (d > 0 ? (int64_t)kp[u] : -1) + 1;
+                hi = d < n ? (int64_t)min(kc[u], nb) : (int64_t)nb;
+            }
+            const bool big = hi - lo >= 8;
+            if (!big)
+                for (int64_t b = lo; b <= hi; b++) offsets[b] = (uint32_t)d;
+            uint32_t m = __ballot_sync(0xffffffffu, big);
+            while (m) {
+                const int src = __ffs(m) - 1;
+                m &= m - 1;
+                const int64_t s0 = __shfl_sync(0xffffffffu, lo, src), s1 = __shfl_sync(0xffffffffu, hi, src);
+                const int dv = __shfl_sync(0xffffffffu, d, src);
+                for (int64_t b = s0 + lane; b <= s1; b += 32) offsets[b] = (uint32_t)dv;
+            }
+            if (d < n && kc[u] < nb) {
+                xy[d] = make_float2(__uint_as_float(r[u].x), __uint_as_float(r[u].y));
+                rng[d] = make_uint2(r[u].z, r[u].w);
+            }
         }
     }
 }
@@ -397,22 +418,38 @@ int bin_points(kde_ctx* c, const double* d_x, const double* d_y, int64_t n64) {
     const Geom& g = c->g;
     cudaStream_t s = c->stream;
     const uint32_t nb = (uint32_t)g.nbx * (uint32_t)g.nby;
-    int bits = 1;  // LSD passes over the key bits of [0, nb]
-    while ((1ull << bits) <= nb) bits++;
-    const int passes = (bits + kRsMaxBits - 1) / kRsMaxBits;
-    const int dbits = (bits + passes - 1) / passes;
-    const uint32_t dmask = (1u << dbits) - 1u;
-    const int nbins = (int)dmask + 1;
+    // LSD passes over the keys [0, nb] (nb = dropped).  The real keys [0, nb) need kb bits;
+    // passes = ceil(kb / 11), digits of db = ceil(kb / passes) bits, and the LAST pass takes
+    // all the remaining high bits, key >> shift in [0, nb >> shift] -- a digit set of
+    // (nb >> shift) + 1 that holds the dropped sentinel without an extra pass (C4: 2^20
+    // buckets -> 1024 + 1025 digits, two passes instead of three).
+    int kb = 1;
+    while ((1ull << kb) < nb) kb++;
+    const int passes = (kb + kRsMaxBits - 1) / kRsMaxBits;
+    const int dbits = (kb + passes - 1) / passes;
+    auto pass_bins = [&](int ps) {
+        return ps == passes - 1 ? (int)(nb >> (ps * dbits)) + 1 : 1 << dbits;
+    };
+    auto pass_mask = [&](int ps) { return ps == passes - 1 ? 0xffffffffu : (1u << dbits) - 1u; };
+    int nbins = 0;  // the largest digit set
+    for (int ps = 0; ps < passes; ps++) nbins = std::max(nbins, pass_bins(ps));
+    const uint32_t dmask0 = pass_mask(0);
+    const int nbins0 = pass_bins(0);
     // tuning knobs (A/B experiments): KDE_RS_ROUNDS = 8|16 forces the tile rounds,
     // KDE_RS_STAGED = the largest digit count that stages the tile in shared memory
     static const int env_rounds = getenv("KDE_RS_ROUNDS") ? atoi(getenv("KDE_RS_ROUNDS")) : 0;
-    static const int env_staged = getenv("KDE_RS_STAGED") ? atoi(getenv("KDE_RS_STAGED")) : 256;
+    static const int env_staged = getenv("KDE_RS_STAGED") ? atoi(getenv("KDE_RS_STAGED")) : 520;
     // default: 4096-key tiles from 8 M points on (measured: C4 binning 0.96 -> 0.91 ms; C2
-    // prefers 2048-key tiles: more CTAs for its 2 M keys)
-    const int rounds = (env_rounds == 8 || env_rounds == 16) ? std::max(env_rounds, nbins / 64)
-                       : (n >= (8 << 20) ? std::max(16, nbins / 64) : rs_rounds(nbins));
+    // prefers 2048-key tiles: more CTAs for its 2 M keys); tiles hold >= 4 keys per digit
+    const int rounds = (env_rounds == 8 || env_rounds == 16) ? std::max(env_rounds, rs_rounds(nbins))
+                       : (n >= (8 << 20) ? std::max(16, rs_rounds(nbins)) : rs_rounds(nbins));
+    if (rounds != 8 && rounds != 16 && rounds != 32) {
+        set_error("binning: %d digits per pass not supported", nbins);
+        return KDE_EUNSUPPORTED;
+    }
     const int tile = kRsThreads * rounds;
     const int nblk = (n + tile - 1) / tile;
+    const int hstride = (nblk + 3) & ~3;  // histogram rows: 16-byte aligned (rs_scan_digits)
     if (n64 > pb.cap || pb.key[0] == nullptr) {
         const int64_t cap = n64 > 1024 ? n64 : 1024;
         int rc = KDE_OK;
@@ -426,52 +463,57 @@ int bin_points(kde_ctx* c, const double* d_x, const double* d_y, int64_t n64) {
         if (rc) return KDE_ENOMEM;
         pb.cap = cap;
     }
-    const int64_t hneed = (int64_t)nbins * (nblk > 0 ? nblk : 1);
+    const int64_t hneed = (int64_t)nbins * (hstride > 0 ? hstride : 4);
     if (hneed > pb.hist_cap) {
         if (grow((void**)&pb.hist, sizeof(uint32_t) * hneed)) return KDE_ENOMEM;
-        if (grow((void**)&pb.scan_tmp, sizeof(uint32_t) * 2048)) return KDE_ENOMEM;  // digit totals
+        if (grow((void**)&pb.scan_tmp, sizeof(uint32_t) * 4096)) return KDE_ENOMEM;  // digit totals
         pb.hist_cap = hneed;
     }
     cudaMemsetAsync(c->d_stats, 0, 3 * sizeof(unsigned long long), s);
     if (n > 0) {
         const size_t up_smem = sizeof(uint32_t) * nbins;
         // small digit sets scatter short runs: stage the tile digit-sorted in shared memory
-        // and write it out coalesced; large ones (>= 512 digits) scatter directly
-        const bool staged = nbins <= env_staged;
-        const size_t dn_smem =
-            sizeof(uint32_t) * (2 * nbins + (staged ? 2 * tile : 0)) + sizeof(uint16_t) * 8 * nbins;
+        // and write it out coalesced; large ones scatter directly
+        auto dn_smem = [&](int nbp, bool stg) {
+            return sizeof(uint32_t) * (2 * nbp + (stg ? 2 * tile : 0)) + sizeof(uint16_t) * 8 * nbp;
+        };
         {   // the shared-memory opt-in is per device and cheap: set it on every load (no
-            // process-global state).  Largest case: 1024 digits, tile 4096, staged.
-            const int mx = (int)(sizeof(uint32_t) * (2 * 1024 + 2 * 4096) + sizeof(uint16_t) * 8 * 1024);
+            // process-global state).  Largest case: 2049 digits, tile 8192.
+            const int mx = (int)std::max(dn_smem(2049, false), dn_smem(520, true));
             cudaFuncSetAttribute(rs_downsweep<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
             cudaFuncSetAttribute(rs_downsweep<true, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
             cudaFuncSetAttribute(rs_downsweep<false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
             cudaFuncSetAttribute(rs_downsweep<false, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+            cudaFuncSetAttribute(rs_downsweep<false, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         }
-        bin_convert_kernel<<<nblk, kRsThreads, up_smem, s>>>(d_x, d_y, n, g, nb, pb.key[0], pb.rec,
-                                                             c->d_stats, dmask, pb.hist, nblk, rounds);
+        bin_convert_kernel<<<nblk, kRsThreads, sizeof(uint32_t) * nbins0, s>>>(
+            d_x, d_y, n, g, nb, pb.key[0], pb.rec, c->d_stats, dmask0, nbins0, pb.hist, hstride, rounds);
         c->launches += 1;
         int cur = 0;
         for (int ps = 0; ps < passes; ps++) {
             const int shift = ps * dbits;
+            const uint32_t dmask = pass_mask(ps);
+            const int nbp = pass_bins(ps);
             if (ps > 0) {
-                rs_upsweep<<<nblk, kRsThreads, up_smem, s>>>(pb.key[cur], n, shift, dmask, pb.hist, nblk, rounds);
+                rs_upsweep<<<nblk, kRsThreads, sizeof(uint32_t) * nbp, s>>>(pb.key[cur], n, shift, dmask, nbp,
+                                                                           pb.hist, hstride, rounds);
                 c->launches += 1;
             }
-            rs_scan_digits<<<nbins, 256, 0, s>>>(pb.hist, nbins, nblk, pb.scan_tmp);
+            rs_scan_digits<<<nbp, 256, 0, s>>>(pb.hist, nbp, nblk, hstride, pb.scan_tmp);
+            const bool staged = nbp <= env_staged && rounds <= 16;
             auto dsw = staged ? (rounds == 8 ? rs_downsweep<true, 8> : rs_downsweep<true, 16>)
-                              : (rounds == 8 ? rs_downsweep<false, 8> : rs_downsweep<false, 16>);
-            dsw<<<nblk, kRsThreads, dn_smem, s>>>(pb.key[cur], ps == 0 ? nullptr : pb.val[cur], pb.key[cur ^ 1],
-                                                  pb.val[cur ^ 1], n, shift, dmask, pb.hist, pb.scan_tmp, nblk);
+                              : (rounds == 8 ? rs_downsweep<false, 8>
+                                             : rounds == 16 ? rs_downsweep<false, 16> : rs_downsweep<false, 32>);
+            dsw<<<nblk, kRsThreads, dn_smem(nbp, staged), s>>>(pb.key[cur], ps == 0 ? nullptr : pb.val[cur],
+                                                                 pb.key[cur ^ 1], pb.val[cur ^ 1], n, shift, dmask,
+                                                                 nbp, pb.hist, pb.scan_tmp, hstride);
             c->launches += 2;
             cur ^= 1;
         }
         pb.perm = pb.val[cur];
-        const int og = (n + 1 + 255) / 256 < 148 * 16 ? (n + 1 + 255) / 256 : 148 * 16;
-        offsets_kernel<<<og, 256, 0, s>>>(pb.key[cur], n, nb, c->d_offsets);
-        const int gg = (n + 1023) / 1024 < 148 * 8 ? (n + 1023) / 1024 : 148 * 8;
-        gather_kernel<<<gg, 256, 0, s>>>(pb.rec, pb.perm, c->d_offsets, nb, pb.xy, pb.rng);
-        c->launches += 2;
+        const int gg = (n + 1 + 1023) / 1024 < 148 * 8 ? (n + 1 + 1023) / 1024 : 148 * 8;
+        gather_offsets_kernel<<<gg, 256, 0, s>>>(pb.rec, pb.perm, pb.key[cur], n, nb, c->d_offsets, pb.xy, pb.rng);
+        c->launches += 1;
     } else {
         cudaMemsetAsync(c->d_offsets, 0, sizeof(uint32_t) * (nb + 1), s);
         pb.perm = pb.val[0];
