@@ -438,7 +438,7 @@ int bin_points(kde_ctx* c, const double* d_x, const double* d_y, int64_t n64) {
     // tuning knobs (A/B experiments): KDE_RS_ROUNDS = 8|16 forces the tile rounds,
     // KDE_RS_STAGED = the largest digit count that stages the tile in shared memory
     static const int env_rounds = getenv("KDE_RS_ROUNDS") ? atoi(getenv("KDE_RS_ROUNDS")) : 0;
-    static const int env_staged = getenv("KDE_RS_STAGED") ? atoi(getenv("KDE_RS_STAGED")) : 520;
+    static const int env_staged = getenv("KDE_RS_STAGED") ? atoi(getenv("KDE_RS_STAGED")) : 1100;
     // default: 4096-key tiles from 8 M points on (measured: C4 binning 0.96 -> 0.91 ms; C2
     // prefers 2048-key tiles: more CTAs for its 2 M keys); tiles hold >= 4 keys per digit
     const int rounds = (env_rounds == 8 || env_rounds == 16) ? std::max(env_rounds, rs_rounds(nbins))
@@ -479,7 +479,7 @@ int bin_points(kde_ctx* c, const double* d_x, const double* d_y, int64_t n64) {
         };
         {   // the shared-memory opt-in is per device and cheap: set it on every load (no
             // process-global state).  Largest case: 2049 digits, tile 8192.
-            const int mx = (int)std::max(dn_smem(2049, false), dn_smem(520, true));
+            const int mx = (int)std::max(dn_smem(2049, false), dn_smem(1100, true));
             cudaFuncSetAttribute(rs_downsweep<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
             cudaFuncSetAttribute(rs_downsweep<true, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
             cudaFuncSetAttribute(rs_downsweep<false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
