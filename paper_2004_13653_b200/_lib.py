@@ -170,7 +170,7 @@ def kde_snap(ctx: int, x, y, label, out, counts=None, stream: int | None = None)
     if int(y.shape[0]) != n or (label is not None and int(label.shape[0]) != n):
         raise ValueError("x, y and label lengths differ")
     shp = _SHAPES.get(ctx)
-    npx = shp[1] * shp[2] if shp else 0
+    npx = shp[0] * shp[2] if shp else 0  # (a banded context is rejected by the C call itself)
     _check_out(ctx, out, npx, "out")
     if counts is not None:
         _check_out(ctx, counts, npx, "counts", ("torch.int32", "torch.uint32"))

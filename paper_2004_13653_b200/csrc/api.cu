@@ -99,8 +99,10 @@ static void plan_geometry_tc(EvalPlan& pl, const Geom& g, bool product) {
                                         // chunks measured slower: 5 CTAs/SM instead of 8)
 }
 
-static int alloc_plan(EvalPlan& pl) {
+static int alloc_plan(EvalPlan& pl, const Geom& g) {
     if (!pl.enabled) return KDE_OK;
+    pl.tfx = (g.W + kCombTile - 1) / kCombTile;
+    pl.tfy = (g.re - g.rb + kCombTile - 1) / kCombTile;
     const size_t ng = (size_t)pl.pg.ngroups();
     const size_t nblk = (size_t)plan_nblk(pl.pg);
     cudaError_t e = cudaMalloc(&pl.d_local, sizeof(uint64_t) * nblk * 1024);
@@ -108,6 +110,7 @@ static int alloc_plan(EvalPlan& pl) {
     if (e == cudaSuccess) e = cudaMalloc(&pl.d_group, sizeof(int2) * (ng > 0 ? ng : 1));
     if (e == cudaSuccess) e = cudaMalloc(&pl.d_totals, sizeof(int) * kTotInts);
     if (e == cudaSuccess) e = cudaMalloc(&pl.d_hot, sizeof(int) * (ng > 0 ? ng : 1));
+    if (e == cudaSuccess) e = cudaMalloc(&pl.d_tflag, (size_t)pl.tfx * pl.tfy);
     if (e != cudaSuccess) {
         cudaGetLastError();
         set_error("kde_create: plan allocation failed");
@@ -173,6 +176,7 @@ static void free_plan(EvalPlan& pl) {
     cudaFree(pl.d_group);
     cudaFree(pl.d_totals);
     cudaFree(pl.d_hot);
+    cudaFree(pl.d_tflag);
     cudaFree(pl.d_items);
     cudaFree(pl.d_splat);
     pl = EvalPlan();
@@ -321,7 +325,7 @@ int kde_create(const kde_params* p, kde_ctx** out) {
         return cuda_fail(e, "kde_create: allocation");
     }
     for (int p = 0; p < 2; p++)
-        if (alloc_plan(c->plan[p])) {
+        if (alloc_plan(c->plan[p], g)) {
             kde_free(c);
             return KDE_ENOMEM;
         }

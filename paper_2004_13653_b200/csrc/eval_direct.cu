@@ -361,6 +361,7 @@ struct CombineArgs {
     Geom g;
     PathGeom pg;
     const int2* __restrict__ group;  // per group: (first segment, #segments)
+    const uint8_t* __restrict__ tflag;  // per tile: a planned group's window meets it
     const float* __restrict__ splat;
     float* __restrict__ out;
     const unsigned long long* __restrict__ stats;  // n_finite = stats[0] (device)
@@ -374,6 +375,12 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineArgs a) {
     const PathGeom& pg = a.pg;
     const int X0 = blockIdx.x * kCombTile, Y0 = g.rb + blockIdx.y * kCombTile;
     const int Y1 = min(Y0 + kCombTile, g.re) - 1, X1 = X0 + kCombTile - 1;
+    if (!a.tflag[(size_t)blockIdx.y * gridDim.x + blockIdx.x]) {  // no group reaches the tile: zeros
+        const int i = X0 + (threadIdx.x & 31);
+        if (i < g.W)
+            for (int j = Y0 + (threadIdx.x >> 5); j <= Y1; j += 8) a.out[(size_t)(j - g.rb) * g.W + i] = 0.f;
+        return;
+    }
     const int F = g.F;
     const int gxa = max(floor_div(X0 - F, pg.px), 0), gxb = min(floor_div(X1 + F, pg.px), pg.ngx - 1);
     const int gya = max(floor_div(Y0 - F, pg.py), 0), gyb = min(floor_div(Y1 + F, pg.py), pg.ngy - 1);
@@ -516,6 +523,7 @@ int launch_combine(kde_ctx* c, const EvalPlan& pl, float* out, cudaStream_t s) {
     a.g = g;
     a.pg = pl.pg;
     a.group = pl.d_group;
+    a.tflag = pl.d_tflag;
     a.splat = pl.d_splat;
     a.out = out;
     a.stats = c->d_stats;

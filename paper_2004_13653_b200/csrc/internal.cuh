@@ -113,6 +113,9 @@ struct EvalPlan {
     int2* d_group = nullptr;                   // per group: (first segment, #segments)
     int* d_totals = nullptr;                   // see kTot*
     int* d_hot = nullptr;                      // groups with > 1 segment (segment reduce)
+    uint8_t* d_tflag = nullptr;                // per combine tile of the band: 1 if a planned
+                                               // group's window meets it (else it is all zero)
+    int tfx = 0, tfy = 0;                      // combine tiles (columns, band rows)
     int4* d_items = nullptr;                   // (group, k0, k1, slot)
     int64_t items_cap = 0;
     float* d_splat = nullptr;

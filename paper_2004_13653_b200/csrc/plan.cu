@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_blocks_kernel(uint64_t* __r
 __global__ void __launch_bounds__(kPlanThreads) plan_finish_kernel(
     const Geom g, const PathGeom pg, const uint32_t* __restrict__ off, const uint64_t* __restrict__ local,
     const uint64_t* __restrict__ bsum, int nblk, int2* __restrict__ group, int4* __restrict__ items,
-    int* __restrict__ totals, int* __restrict__ hot) {
+    int* __restrict__ totals, int* __restrict__ hot, uint8_t* __restrict__ tflag, int tfx, int tfy) {
     const uint64_t T = bsum[nblk];
     const int TF = (int)(T >> 32);
     const int nsub = pg.nsub(), ng = pg.ngroups();
@@ -133,6 +133,14 @@ __global__ void __launch_bounds__(kPlanThreads) plan_finish_kernel(
             group[i] = make_int2(fs + ps, nf + np);  // first segment (numbered group by group)
             gst = (int)off[(i % pg.ngx) * g.nby + (i / pg.ngx) * pg.s];  // group's first position
             if (nf + np > 1) hot[atomicAdd(&totals[kTotHot], 1)] = i;  // split group: segment reduce
+            if (nf + np > 0) {  // the combine tiles (band-relative) its window meets are non-empty
+                const int wx0 = (i % pg.ngx) * pg.px - g.F, wy0 = (i / pg.ngx) * pg.py - g.F - g.rb;
+                const int tx0 = max(wx0, 0) / kCombTile, tx1 = min((wx0 + pg.ww - 1) / kCombTile, tfx - 1);
+                const int ty0 = max(wy0, 0) / kCombTile;
+                const int ty1 = wy0 + pg.wh - 1 >= 0 ? min((wy0 + pg.wh - 1) / kCombTile, tfy - 1) : -1;
+                for (int ty = ty0; ty <= ty1; ty++)
+                    for (int tx = tx0; tx <= tx1; tx++) tflag[(size_t)ty * tfx + tx] = 1;
+            }
             chunks += ((uint32_t)nf * (pg.seg_pts / pg.chunk_pts) +
                        ((cnt % pg.seg_pts) + pg.chunk_pts - 1) / pg.chunk_pts) * (uint32_t)nsub;
         }
@@ -193,10 +201,12 @@ int plan_device(kde_ctx* c, EvalPlan& pl, cudaStream_t s) {
     const PathGeom& pg = pl.pg;
     const int nblk = plan_nblk(pg);
     cudaMemsetAsync(pl.d_totals, 0, sizeof(int) * kTotInts, s);  // counters start at zero
+    cudaMemsetAsync(pl.d_tflag, 0, (size_t)pl.tfx * pl.tfy, s);
     plan_local_kernel<<<nblk, kPlanThreads, 0, s>>>(c->g, pg, c->d_offsets, pl.d_local, pl.d_bsum);
     plan_blocks_kernel<<<1, kPlanThreads, 0, s>>>(pl.d_bsum, nblk);
     plan_finish_kernel<<<nblk, kPlanThreads, 0, s>>>(c->g, pg, c->d_offsets, pl.d_local, pl.d_bsum,
-                                                     nblk, pl.d_group, pl.d_items, pl.d_totals, pl.d_hot);
+                                                     nblk, pl.d_group, pl.d_items, pl.d_totals, pl.d_hot,
+                                                     pl.d_tflag, pl.tfx, pl.tfy);
     c->launches += 3;
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "plan launch");
