@@ -374,3 +374,21 @@ def test_tensor_split_full_size_sampled_C2():
     pi, pj = sample_pixels(W, W, (0, W), gpu=gpu, tiles=[(hx, hy, 64, 64)], n_random=2048, seed=seed)
     ref, _ = oracle.kde_pixels(_grid(c, kernel=6), c["x"], c["y"], pi, pj, threads=THREADS)
     assert np.abs(gpu[pj, pi] - ref).max() <= TOL_DIRECT * ref.max()
+
+
+# --- fp16 operand range (R11): a cutoff far past fp16's normal range -----------------
+@pytest.mark.parametrize("hpx", [1.5, 4.0])
+def test_tensor_fp16_range_cutoff9(hpx):
+    """The tensor path rounds 1-D factors exp(-s^2/2) to fp16.  At cutoff 9 the smallest kept
+    factor is exp(-40.5) = 2.6e-18, far below fp16's smallest subnormal (6e-8): such factors
+    flush to 0 (or a subnormal).  Each lost product is < 6e-8 of the peak pair (1 x 1), so the
+    2e-3 * max bar holds unless ~3e4 far-tail pairs outweigh the peak pixel -- checked here on
+    an estuary cloud (hot lanes + sparse tails) at h = 1.5 px (the per-factor exp2 branch of
+    the recurrence guard) and 4 px."""
+    c = case("estuary", 100_000, 300, hpx, seed=31, H=260)
+    k = _tc(c, cutoff=9.0)
+    gpu = k.eval("tensor").cpu().numpy()
+    ref, _ = oracle.kde_raster(_grid(c, kernel=6, cutoff=9.0), c["x"], c["y"], threads=THREADS)
+    assert _err(gpu, ref) <= TOL_TENSOR
+    d = k.eval("direct").cpu().numpy()
+    assert _err(d, ref) <= TOL_DIRECT
