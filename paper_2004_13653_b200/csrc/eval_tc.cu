@@ -153,7 +153,7 @@ __device__ __forceinline__ void sts128(uint32_t saddr, uint4 v) {
 // residual lo = RN16(f - RN16(f)) into a second operand plane lo_off bytes further, so that
 // A_hi B_hi + A_hi B_lo + A_lo B_hi carries ~22 mantissa bits (the lo*lo term is 2^-22 of
 // the product): the fp32 path's 1e-5 bar on the tensor pipe.
-template <int K, bool SPLIT>
+template <int K, bool SPLIT, bool REC>
 __device__ __forceinline__ void kern_unit(uint32_t dst, uint32_t lo_off, int c0, float ph, int lo, int span,
                                           const TcArgs& a) {
     const int l0 = max(lo - c0, 0), h0 = min(lo + span - c0, 7);
@@ -163,7 +163,7 @@ __device__ __forceinline__ void kern_unit(uint32_t dst, uint32_t lo_off, int c0,
         const uint32_t m = (2u << h0) - (1u << l0);
         const float d0 = (float)c0 - ph;
         float f[8];
-        if constexpr (K == KDE_GAUSSIAN) {
+        if constexpr (K == KDE_GAUSSIAN && REC) {
             float gv = ex2_ftz(d0 * d0 * a.kq);
             float r = ex2_ftz(fmaf(2.0f, d0, 1.0f) * a.kq);
 #pragma unroll
@@ -202,7 +202,7 @@ __device__ __forceinline__ void kern_unit(uint32_t dst, uint32_t lo_off, int c0,
     if constexpr (SPLIT) sts128(dst + lo_off, ol);
 }
 
-template <int H, int K, bool SPLIT>
+template <int H, int K, bool SPLIT, bool REC>
 __global__ void __launch_bounds__(kTcThreads, TcShape<H>::kMinBlocks) tc_splat_kernel(const TcArgs a) {
     using SH = TcShape<H>;
     constexpr int kTcChunk = SH::kChunk, kTcABytes = SH::kABytes, kSBO = SH::kSBO;
@@ -336,12 +336,12 @@ __global__ void __launch_bounds__(kTcThreads, TcShape<H>::kMinBlocks) tc_splat_k
                 const int u = warp + 4 * j;
 #pragma unroll
                 for (int h = 0; h < H; h++)
-                    kern_unit<K, SPLIT>(ab + u * kSBO + h * 512, kTcABytes, u * 8, pyh[h], jlo[h], jspan[h], a);
+                    kern_unit<K, SPLIT, REC>(ab + u * kSBO + h * 512, kTcABytes, u * 8, pyh[h], jlo[h], jspan[h], a);
             }
             for (int u = warp; u < nbu; u += 4)  // B: N/8 column units
 #pragma unroll
                 for (int h = 0; h < H; h++)
-                    kern_unit<K, SPLIT>(bb + u * kSBO + h * 512, bbytes, u * 8, pxh[h], ilo[h], ispan[h], a);
+                    kern_unit<K, SPLIT, REC>(bb + u * kSBO + h * 512, bbytes, u * 8, pxh[h], ilo[h], ispan[h], a);
             fence_async_smem();
             __syncthreads();
             if (t == kIssuer) {  // warp 3 generates the fewest B units
@@ -387,17 +387,17 @@ __global__ void __launch_bounds__(kTcThreads, TcShape<H>::kMinBlocks) tc_splat_k
     }
 }
 
-template <int H, int K, bool SPLIT>
+template <int H, int K, bool SPLIT, bool REC>
 static void launch_tc_h(kde_ctx* c, EvalPlan& pl, const TcArgs& a, cudaStream_t s) {
     const size_t smem =
         (SPLIT ? 2 : 1) * (2 * (size_t)TcShape<H>::kABytes + 2 * (size_t)a.n * TcShape<H>::kChunk * 2) + 1024;
     int& grid = SPLIT ? pl.grid_split : pl.grid;
     if (grid <= 0) {
-        cudaFuncSetAttribute(tc_splat_kernel<H, K, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(tc_splat_kernel<H, K, SPLIT, REC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int nsm = 148, per = 0;
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->p.device);
         const cudaError_t oe =
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tc_splat_kernel<H, K, SPLIT>, kTcThreads, smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tc_splat_kernel<H, K, SPLIT, REC>, kTcThreads, smem);
         if (getenv("KDE_DEBUG"))
             fprintf(stderr, "[kde] tc occupancy query: err=%d per=%d smem=%zu\n", (int)oe, per, smem);
         // (the occupancy API reports 1 CTA/SM for this kernel; size from the real limits:
@@ -411,7 +411,7 @@ static void launch_tc_h(kde_ctx* c, EvalPlan& pl, const TcArgs& a, cudaStream_t 
     }
     cudaMemsetAsync(pl.d_totals + kTotQueue, 0, sizeof(int), s);  // work-queue head
     tmark(c, 3, s);
-    tc_splat_kernel<H, K, SPLIT><<<grid, kTcThreads, smem, s>>>(a);  // persistent; item count on device
+    tc_splat_kernel<H, K, SPLIT, REC><<<grid, kTcThreads, smem, s>>>(a);  // persistent; item count on device
 }
 
 int launch_tc(kde_ctx* c, float* out, cudaStream_t s, bool split) {
@@ -433,14 +433,24 @@ int launch_tc(kde_ctx* c, float* out, cudaStream_t s, bool split) {
     a.q2 = (float)exp2(2.0 * (double)a.kq);
     a.twoc = (float)(2.0 * cos(3.14159265358979323846 / (2.0 * c->hpx)));
     a.k = make_kconst(c->hpx);
-    // chunk_pts is 32 (H = 1): 64-point chunks measured slower
+    // chunk_pts is 32 (H = 1): 64-point chunks measured slower.  The Gaussian's
+    // recurrence starts at a unit's first pixel, up to F + B + 7.5 px from the point: while
+    // 2^(kq d^2) stays a normal float there it is exact-ratio; otherwise (small h with a
+    // large cutoff) one exp2 per factor (REC = false).
+    const double dmax = c->g.F + c->g.B + 8.0;
+    const bool rec = -(double)a.kq * dmax * dmax < 120.0;
     using Fn = void (*)(kde_ctx*, EvalPlan&, const TcArgs&, cudaStream_t);
     static const Fn kLaunch[2][8] = {
-        {launch_tc_h<1, 0, false>, launch_tc_h<1, 1, false>, launch_tc_h<1, 2, false>, launch_tc_h<1, 3, false>,
-         launch_tc_h<1, 4, false>, launch_tc_h<1, 5, false>, launch_tc_h<1, 6, false>, launch_tc_h<1, 7, false>},
-        {launch_tc_h<1, 0, true>, launch_tc_h<1, 1, true>, launch_tc_h<1, 2, true>, launch_tc_h<1, 3, true>,
-         launch_tc_h<1, 4, true>, launch_tc_h<1, 5, true>, launch_tc_h<1, 6, true>, launch_tc_h<1, 7, true>}};
-    kLaunch[split ? 1 : 0][c->kern](c, pl, a, s);
+        {launch_tc_h<1, 0, false, true>, launch_tc_h<1, 1, false, true>, launch_tc_h<1, 2, false, true>,
+         launch_tc_h<1, 3, false, true>, launch_tc_h<1, 4, false, true>, launch_tc_h<1, 5, false, true>,
+         launch_tc_h<1, 6, false, true>, launch_tc_h<1, 7, false, true>},
+        {launch_tc_h<1, 0, true, true>, launch_tc_h<1, 1, true, true>, launch_tc_h<1, 2, true, true>,
+         launch_tc_h<1, 3, true, true>, launch_tc_h<1, 4, true, true>, launch_tc_h<1, 5, true, true>,
+         launch_tc_h<1, 6, true, true>, launch_tc_h<1, 7, true, true>}};
+    if (c->kern == KDE_GAUSSIAN && !rec)
+        (split ? launch_tc_h<1, 6, true, false> : launch_tc_h<1, 6, false, false>)(c, pl, a, s);
+    else
+        kLaunch[split ? 1 : 0][c->kern](c, pl, a, s);
     c->launches += 1;
     tmark(c, 4, s);
     launch_combine(c, pl, out, s);
