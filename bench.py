@@ -216,44 +216,55 @@ def run_ours(args):
     W = H = cfg["W"]
     cloud, x0, y0, res = _gen(cfg, args.dp_eps, dev)
     n_pts = len(cloud.x)
-    from paper_2004_13653_b200.dist import assemble, plan_bands
-    bands = plan_bands(H, ws, 256)
-    rows = bands[rank] if ws > 1 else (0, H)
-    nrows = max(re - rb for rb, re in bands) if ws > 1 else H
+    from paper_2004_13653_b200 import dist as kdist
+    xfull = torch.from_numpy(cloud.x).to(dev)
+    yfull = torch.from_numpy(cloud.y).to(dev)
+    if ws > 1:
+        # a6: every rank holds 1/P of the points (NaN-padded shard) and the
+        # step all-gathers them over NVLink; the bands are cut at equal shares of the useful-pair
+        # workload (the all-reduced per-row histogram convolved with the support), once
+        xs, ys = kdist.shard_points(xfull, yfull, rank, ws)
+        R = (cfg["cutoff"] if cfg["kernel"] == "gaussian" else min(cfg["cutoff"], 1.0)) * cfg["hpx"]
+        bands = kdist.balanced_bands_for(ys, y0, res, H, R, ws)
+        del xfull, yfull
+    else:
+        xs, ys, bands = xfull, yfull, [(0, H)]
+    rows = bands[rank]
+    nrows = max(re - rb for rb, re in bands)
     k = KDE(x0, y0, res, W, H, cfg["hpx"] * res, kernel=cfg["kernel"], cutoff=cfg["cutoff"],
-            radial=cfg["radial"], rows=rows if ws > 1 else None, device=local)
-    xd = torch.from_numpy(cloud.x).to(dev)
-    yd = torch.from_numpy(cloud.y).to(dev)
+            radial=cfg["radial"], rows=rows if ws > 1 else None, device=local) if rows[1] > rows[0] else None
     out = torch.zeros((nrows, W), dtype=torch.float32, device=dev)
     myrows = rows[1] - rows[0]
+
+    def points(xa, ya):
+        return kdist.gather_points(xa, ya) if ws > 1 else (xa, ya)
+
+    def assemble(o):
+        return kdist.gather_to_root(o, bands, H, W) if ws > 1 else o  # a6: NCCL gather to rank 0
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     path = args.path
     if path == "auto":
-        path = "tensor"
-        try:
-            k.load(xd, yd)
-            k.eval("tensor", out[:myrows])
-        except KdeError:
-            path = "direct"
+        path = "tensor" if (not cfg["radial"]) else "direct"  # the tensor path takes product kernels
 
     def step():
-        k.load(xd, yd)
-        k.eval(path, out[:myrows])
-        if ws > 1:
-            return assemble(out, bands, H, W)  # a6: NCCL all-gather of the row bands
-        return out
+        x, y = points(xs, ys)
+        if k is not None:
+            k.load(x, y)
+            k.eval(path, out[:myrows])
+        return assemble(out)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    st = k.stats()
+    st = k.stats() if k is not None else {"useful_pairs": 0, "kernel_launches": 0, "tc_mma_flops": 0}
+    kstats = (lambda: k.stats()) if k is not None else (lambda: st)
 
     # --- timed region: K steps, L2 flushed before each, events on the launching stream
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
-    launches0 = k.stats()["kernel_launches"]
+    launches0 = kstats()["kernel_launches"]
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -266,7 +277,7 @@ def run_ours(args):
         torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
-    launches = k.stats()["kernel_launches"] - launches0
+    launches = kstats()["kernel_launches"] - launches0
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms = sum(step_ms) / len(step_ms)
     step_stats = {"mean": round(ms, 4), "median": round(statistics.median(step_ms), 4),
@@ -274,18 +285,21 @@ def run_ours(args):
 
     # --- per-phase device times (CUDA events recorded by libkde on the streams its
     # kernels run on), for the dominant kernel's roofline
-    k.set_timing(True)
     ph = {"bin_ms": [], "plan_ms": [], "main_ms": [], "combine_ms": []}
-    for i in range(args.steps):
-        flush.zero_()
-        torch.cuda.synchronize()
-        k.load(xd, yd)
-        k.eval(path, out[:myrows])
-        t = k.timing()
-        for key in ph:
-            ph[key].append(t[key])
-    k.set_timing(False)
-    phases = {key: round(sum(v) / len(v), 4) for key, v in ph.items()}
+    if k is not None:
+        xg, yg = points(xs, ys)
+        k.set_timing(True)
+        for i in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            k.load(xg, yg)
+            k.eval(path, out[:myrows])
+            t = k.timing()
+            for key in ph:
+                ph[key].append(t[key])
+        k.set_timing(False)
+        del xg, yg
+    phases = {key: round(sum(v) / len(v), 4) if v else 0.0 for key, v in ph.items()}
     eval_ms = phases["main_ms"]
 
     # --- e2e: the same step through the public API with HOST buffers (pinned): every step
@@ -293,8 +307,10 @@ def run_ours(args):
     # device->host.  Steps are pipelined the way a user streaming batches would: step i's
     # D2H runs on a side stream (double-buffered raster) while step i+1 uploads and bins,
     # so the two PCIe directions overlap.
-    xh = torch.from_numpy(cloud.x).pin_memory()
-    yh = torch.from_numpy(cloud.y).pin_memory()
+    # N > 1: each rank uploads only its 1/P shard of the points, then the all-gather
+    xh = xs.cpu().pin_memory()
+    yh = ys.cpu().pin_memory()
+    xsd, ysd = torch.empty_like(xs), torch.empty_like(ys)
     fullh = [torch.empty((H, W), dtype=torch.float32).pin_memory() for _ in range(2)]
     outs = [torch.zeros((nrows, W), dtype=torch.float32, device=dev) for _ in range(2)]
     d2h = torch.cuda.Stream(dev)
@@ -303,9 +319,17 @@ def run_ours(args):
     def step_e2e(i):
         o = outs[i % 2]
         done_ev[i % 2].synchronize()  # the D2H that last read this buffer has finished
-        k.load(xh, yh)
-        k.eval(path, o[:myrows])
-        full = assemble(o, bands, H, W) if ws > 1 else o
+        if ws > 1:
+            xsd.copy_(xh, non_blocking=True)
+            ysd.copy_(yh, non_blocking=True)
+            x, y = points(xsd, ysd)
+            if k is not None:
+                k.load(x, y)
+        elif k is not None:
+            k.load(xh, yh)  # host buffers straight through the C ABI (H2D inside kde_load_points)
+        if k is not None:
+            k.eval(path, o[:myrows])
+        full = assemble(o)
         ready = torch.cuda.Event()
         ready.record(stream)
         with torch.cuda.stream(d2h):
@@ -325,8 +349,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     e2e = (time.perf_counter() - t0) * 1e3 / args.steps
     # context for e2e: the raw pinned host->device copy of the same 16 B/point, alone
-    dx_ = torch.empty_like(xd)
-    dy_ = torch.empty_like(yd)
+    dx_ = torch.empty_like(xs)
+    dy_ = torch.empty_like(ys)
     h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     dx_.copy_(xh, non_blocking=True)
     torch.cuda.synchronize()
@@ -417,16 +441,17 @@ def run_ours(args):
                    "cutoff": cfg["cutoff"], "kernel": cfg["kernel"],
                    "form": "radial" if cfg["radial"] else "product",
                    "parallelism": f"row-bands x{ws}" if ws > 1 else "single",
+                   "bands": bands if ws > 1 else None,
                    "l2": "flushed (512 MiB write) before every timed step"},
         "pixels_per_s": W * H / (ms * 1e-3),
         "useful_pairs": useful,
         "step_ms_rank0": step_stats,
         "e2e": {"value": useful / (e2e * 1e-3), "unit": UNIT, "ms_per_step": round(e2e, 4),
-                "h2d_bytes_per_step": 16 * n_pts,
+                "h2d_bytes_per_step": 16 * int(xs.shape[0]),
                 "d2h_bytes_per_step": 4 * W * H,
                 "note": "pinned host buffers; step i's D2H overlaps step i+1's H2D (pipelined)",
                 "h2d_alone_ms": round(h2d_ms, 4),
-                "h2d_alone_gbs": round(16 * n_pts / (h2d_ms * 1e-3) / 1e9, 1)},
+                "h2d_alone_gbs": round(16 * int(xs.shape[0]) / (h2d_ms * 1e-3) / 1e9, 1)},
         "gpu_launches": int(launches),
         "phases_ms": phases,
         "clocks": clocks,
@@ -473,7 +498,7 @@ def run_snap(args):
     for _ in range(args.warmup):
         k.snap(xd, yd, ld, out=out, counts=cnt)
     torch.cuda.synchronize()
-    launches0 = k.stats()["kernel_launches"]
+    launches0 = kstats()["kernel_launches"]
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     with ClockSampler(0) as clk:
@@ -483,7 +508,7 @@ def run_snap(args):
             k.snap(xd, yd, ld, out=out, counts=cnt)
             ev[i][1].record(stream)
         torch.cuda.synchronize()
-    launches = k.stats()["kernel_launches"] - launches0
+    launches = kstats()["kernel_launches"] - launches0
     ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
     # e2e: host inputs (pinned), the Eq. 7 matrix read back every step
     xh, yh, lh = (torch.from_numpy(a).pin_memory() for a in (cloud.x, cloud.y, lab))

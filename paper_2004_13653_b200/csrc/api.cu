@@ -557,6 +557,11 @@ int kde_get_bins(const kde_ctx* c, int64_t* offsets, int64_t* perm, float* lx, f
     if (perm) {
         pv.resize(m);
         e = cudaMemcpy(pv.data(), c->pb.perm, sizeof(uint32_t) * m, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess && c->pb.compacted) {  // banded: sorted compacted positions -> input indices
+            std::vector<uint32_t> ci((size_t)c->stats.n_in);
+            e = cudaMemcpy(ci.data(), c->pb.cidx, sizeof(uint32_t) * ci.size(), cudaMemcpyDeviceToHost);
+            for (size_t k = 0; k < m && e == cudaSuccess; k++) pv[k] = ci[pv[k]];
+        }
         for (size_t k = 0; k < m && e == cudaSuccess; k++) perm[k] = (int64_t)pv[k];
     }
     if (e == cudaSuccess && (lx || ly)) {
@@ -737,6 +742,11 @@ void kde_free(kde_ctx* c) {
     cudaFree(pb.rec);
     cudaFree(pb.xy);
     cudaFree(pb.rng);
+    cudaFree(pb.cx);
+    cudaFree(pb.cy);
+    cudaFree(pb.cidx);
+    cudaFree(pb.bcnt);
+    cudaFree(pb.nfin);
     cudaFree(c->d_offsets);
     cudaFree(c->d_stats);
     free_plan(c->plan[0]);

@@ -400,6 +400,92 @@ __global__ void __launch_bounds__(256) gather_offsets_kernel(const uint4* __rest
     }
 }
 
+// ---------------------------------------------------------------------------------
+// Banded contexts (row-band sharding): only the points whose home-bucket row is
+// within the band's reach are binned.  They are compacted IN INPUT ORDER before the sort
+// (per-block counts -> scan -> write), so a rank sorts ~n/P + halo keys instead of all n, and
+// the sort's stability still orders equal keys by original index (the values carried through
+// the sort are compacted positions; cidx maps them back).
+constexpr int kBcThreads = 256, kBcPer = 4, kBcTile = kBcThreads * kBcPer;
+
+__global__ void __launch_bounds__(kBcThreads) band_count_kernel(const double* __restrict__ x,
+                                                                const double* __restrict__ y, int n, Geom g,
+                                                                uint32_t* __restrict__ bcnt,
+                                                                unsigned long long* __restrict__ nfin) {
+    __shared__ uint32_t s_k[kBcThreads / 32], s_f[kBcThreads / 32];
+    uint32_t kept = 0, fin = 0;
+#pragma unroll
+    for (int r = 0; r < kBcPer; r++) {
+        const int i = blockIdx.x * kBcTile + r * kBcThreads + threadIdx.x;
+        if (i < n) {
+            const Binned b = bin_point(x[i], y[i], g, 0u);
+            kept += b.status == 2;
+            fin += b.status > 0;
+        }
+    }
+    kept = __reduce_add_sync(0xffffffffu, kept);
+    fin = __reduce_add_sync(0xffffffffu, fin);
+    if ((threadIdx.x & 31) == 0) {
+        s_k[threadIdx.x >> 5] = kept;
+        s_f[threadIdx.x >> 5] = fin;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t k = 0, f = 0;
+        for (int w = 0; w < kBcThreads / 32; w++) {
+            k += s_k[w];
+            f += s_f[w];
+        }
+        bcnt[blockIdx.x] = k;
+        if (f) atomicAdd(nfin, (unsigned long long)f);
+    }
+}
+
+__global__ void __launch_bounds__(kBcThreads) band_compact_kernel(const double* __restrict__ x,
+                                                                  const double* __restrict__ y, int n, Geom g,
+                                                                  const uint32_t* __restrict__ boff,
+                                                                  double* __restrict__ cx, double* __restrict__ cy,
+                                                                  uint32_t* __restrict__ cidx) {
+    __shared__ uint32_t s_w[kBcThreads / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t base = boff[blockIdx.x];
+#pragma unroll
+    for (int r = 0; r < kBcPer; r++) {  // rounds in input order; within a round, warp order
+        const int i = blockIdx.x * kBcTile + r * kBcThreads + threadIdx.x;
+        double xv = 0.0, yv = 0.0;
+        bool keep = false;
+        if (i < n) {
+            xv = x[i];
+            yv = y[i];
+            keep = bin_point(xv, yv, g, 0u).status == 2;
+        }
+        const uint32_t m = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) s_w[warp] = __popc(m);
+        __syncthreads();
+        uint32_t pre = 0, tot = 0;
+        for (int w = 0; w < kBcThreads / 32; w++) {
+            pre += w < warp ? s_w[w] : 0u;
+            tot += s_w[w];
+        }
+        if (keep) {
+            const uint32_t o = base + pre + __popc(m & ((1u << lane) - 1u));
+            cx[o] = xv;
+            cy[o] = yv;
+            cidx[o] = (uint32_t)i;
+        }
+        base += tot;
+        __syncthreads();
+    }
+}
+
+// after binning a compacted set: n_finite counts every finite point passed in (the
+// normalisation, R4), n_outside the finite ones not binned
+__global__ void band_stats_kernel(unsigned long long* __restrict__ stats, const unsigned long long* __restrict__ nfin,
+                                  uint32_t m) {
+    stats[0] = *nfin;
+    stats[1] = *nfin - (unsigned long long)m;
+}
+
 static int grow(void** p, size_t bytes) {
     if (*p) cudaFree(*p);
     *p = nullptr;
@@ -412,8 +498,54 @@ static int grow(void** p, size_t bytes) {
     return KDE_OK;
 }
 
+static int bin_sorted(kde_ctx* c, const double* d_x, const double* d_y, int n);
+
 int bin_points(kde_ctx* c, const double* d_x, const double* d_y, int64_t n64) {
     const int n = (int)n64;
+    PointBufs& pb = c->pb;
+    const Geom& g = c->g;
+    const bool banded = g.band_lo > 0 || g.band_hi < g.nby - 1;
+    pb.compacted = false;
+    if (!banded || n == 0) return bin_sorted(c, d_x, d_y, n);
+    cudaStream_t s = c->stream;
+    const int nbk = (n + kBcTile - 1) / kBcTile;
+    if (n64 > pb.ccap) {
+        int rc = KDE_OK;
+        rc |= grow((void**)&pb.cx, sizeof(double) * n64);
+        rc |= grow((void**)&pb.cy, sizeof(double) * n64);
+        rc |= grow((void**)&pb.cidx, sizeof(uint32_t) * n64);
+        if (rc) return KDE_ENOMEM;
+        pb.ccap = n64;
+    }
+    if (nbk + 8 > pb.bcap) {
+        if (grow((void**)&pb.bcnt, sizeof(uint32_t) * ((nbk + 8 + 3) & ~3))) return KDE_ENOMEM;
+        if (!pb.nfin && grow((void**)&pb.nfin, sizeof(unsigned long long) * 2)) return KDE_ENOMEM;
+        pb.bcap = nbk + 8;
+    }
+    if (!pb.scan_tmp && grow((void**)&pb.scan_tmp, sizeof(uint32_t) * 4096)) return KDE_ENOMEM;
+    cudaMemsetAsync(pb.nfin, 0, sizeof(unsigned long long), s);
+    band_count_kernel<<<nbk, kBcThreads, 0, s>>>(d_x, d_y, n, g, pb.bcnt, pb.nfin);
+    rs_scan_digits<<<1, 256, 0, s>>>(pb.bcnt, 1, nbk, nbk, pb.scan_tmp);  // one row: block offsets; total = m
+    band_compact_kernel<<<nbk, kBcThreads, 0, s>>>(d_x, d_y, n, g, pb.bcnt, pb.cx, pb.cy, pb.cidx);
+    c->launches += 3;
+    uint32_t m = 0;  // the kept count sizes the sort: one readback per banded load
+    cudaError_t e = cudaMemcpyAsync(c->h_totals + 28, pb.scan_tmp, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "band compaction");
+    m = (uint32_t)c->h_totals[28];
+    const int rc = bin_sorted(c, pb.cx, pb.cy, (int)m);  // sorts compacted positions (cidx: originals)
+    if (rc) return rc;
+    band_stats_kernel<<<1, 1, 0, s>>>(c->d_stats, pb.nfin, m);
+    c->launches += 1;
+    pb.compacted = true;
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "band compaction launch");
+    return KDE_OK;
+}
+
+// a1/a2 over n points (the sort carries each point's position in d_x / d_y)
+static int bin_sorted(kde_ctx* c, const double* d_x, const double* d_y, int n) {
+    const int64_t n64 = n;
     PointBufs& pb = c->pb;
     const Geom& g = c->g;
     cudaStream_t s = c->stream;

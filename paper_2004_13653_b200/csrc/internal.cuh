@@ -59,6 +59,13 @@ struct PointBufs {
     float2 *xy = nullptr;                      // sorted bucket-local coordinates
     uint2 *rng = nullptr;                      // sorted packed int16 ranges
     uint32_t *perm = nullptr;                  // sorted -> original index (alias)
+    // banded contexts: the points binning keeps, compacted in input order before the sort
+    double *cx = nullptr, *cy = nullptr;       // their coordinates
+    uint32_t *cidx = nullptr;                  // their original indices
+    uint32_t *bcnt = nullptr;                  // per-block kept counts -> offsets
+    unsigned long long *nfin = nullptr;        // finite points (the 1/n normalisation)
+    int64_t ccap = 0, bcap = 0;
+    bool compacted = false;                    // the last load went through the compaction
 };
 
 // Geometry of one evaluation path's work decomposition.  A group is a vertical stack of

@@ -29,7 +29,9 @@ def test_two_rank_row_bands_bitwise(tmp_path):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     v = json.loads(out.read_text())
-    assert v["direct"] and v["tensor"], v
+    assert v["direct"] and v["tensor"] and v["n_finite"], v
+    bands = v["bands"]
+    assert bands[0][0] == 0 and bands[-1][1] == 600 and all(a[1] == b[0] for a, b in zip(bands, bands[1:]))
 
 
 def test_bench_two_ranks_prints_one_line():

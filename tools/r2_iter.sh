@@ -1,6 +1,6 @@
 # round-2 iteration on the GPU: tools/r2_iter.sh "<pytest -k expr>" "<bench configs>" "<paths>"
 sel=$1; cfgs=${2:-"C2 C4"}; paths=${3:-"tensor"}
-if [ -n "$sel" ]; then timeout 900 python -m pytest tests -x -q -m gpu -k "$sel" 2>&1 | tail -3; fi
+if [ -n "$sel" ]; then timeout 900 python -m pytest tests -x -q -m gpu -k "$sel" > gpurun_out/it_pytest.log 2>&1; tail -3 gpurun_out/it_pytest.log; fi
 for c in $cfgs; do for p in $paths; do
   timeout 240 python bench.py --config $c --path $p --no-cpu-baseline --steps 10 --warmup 3 > gpurun_out/it_${c}_$p.json 2> gpurun_out/it_${c}_$p.err
   python -c "
