@@ -408,6 +408,18 @@ __global__ void __launch_bounds__(256) gather_offsets_kernel(const uint4* __rest
 // the sort are compacted positions; cidx maps them back).
 constexpr int kBcThreads = 256, kBcPer = 4, kBcTile = kBcThreads * kBcPer;
 
+// the band filter: finite, and the home-bucket row (bin_point's fp64 v, the same RN
+// operations) within the band's kept rows.  Points that pass but miss the raster are
+// dropped by the convert kernel as usual.
+__device__ __forceinline__ int band_status(double x, double y, const Geom& g) {
+    if (!isfinite(x) || !isfinite(y)) return 0;
+    const double v = __ddiv_rn(__dsub_rn(y, g.y0), g.res);
+    const double fv = floor(v);
+    const int hy = fv < 0.0 ? 0 : (fv > (double)(g.H - 1) ? g.H - 1 : (int)fv);
+    const int by = hy >> g.lgB;
+    return (by < g.band_lo || by > g.band_hi) ? 1 : 2;
+}
+
 __global__ void __launch_bounds__(kBcThreads) band_count_kernel(const double* __restrict__ x,
                                                                 const double* __restrict__ y, int n, Geom g,
                                                                 uint32_t* __restrict__ bcnt,
@@ -418,9 +430,9 @@ __global__ void __launch_bounds__(kBcThreads) band_count_kernel(const double* __
     for (int r = 0; r < kBcPer; r++) {
         const int i = blockIdx.x * kBcTile + r * kBcThreads + threadIdx.x;
         if (i < n) {
-            const Binned b = bin_point(x[i], y[i], g, 0u);
-            kept += b.status == 2;
-            fin += b.status > 0;
+            const int st = band_status(x[i], y[i], g);
+            kept += st == 2;
+            fin += st > 0;
         }
     }
     kept = __reduce_add_sync(0xffffffffu, kept);
@@ -457,7 +469,7 @@ __global__ void __launch_bounds__(kBcThreads) band_compact_kernel(const double* 
         if (i < n) {
             xv = x[i];
             yv = y[i];
-            keep = bin_point(xv, yv, g, 0u).status == 2;
+            keep = band_status(xv, yv, g) == 2;
         }
         const uint32_t m = __ballot_sync(0xffffffffu, keep);
         if (lane == 0) s_w[warp] = __popc(m);
@@ -481,9 +493,9 @@ __global__ void __launch_bounds__(kBcThreads) band_compact_kernel(const double* 
 // after binning a compacted set: n_finite counts every finite point passed in (the
 // normalisation, R4), n_outside the finite ones not binned
 __global__ void band_stats_kernel(unsigned long long* __restrict__ stats, const unsigned long long* __restrict__ nfin,
-                                  uint32_t m) {
+                                  const uint32_t* __restrict__ binned) {
     stats[0] = *nfin;
-    stats[1] = *nfin - (unsigned long long)m;
+    stats[1] = *nfin - (unsigned long long)*binned;
 }
 
 static int grow(void** p, size_t bytes) {
@@ -535,7 +547,7 @@ int bin_points(kde_ctx* c, const double* d_x, const double* d_y, int64_t n64) {
     m = (uint32_t)c->h_totals[28];
     const int rc = bin_sorted(c, pb.cx, pb.cy, (int)m);  // sorts compacted positions (cidx: originals)
     if (rc) return rc;
-    band_stats_kernel<<<1, 1, 0, s>>>(c->d_stats, pb.nfin, m);
+    band_stats_kernel<<<1, 1, 0, s>>>(c->d_stats, pb.nfin, c->d_offsets + (size_t)g.nbx * g.nby);
     c->launches += 1;
     pb.compacted = true;
     e = cudaGetLastError();
