@@ -498,7 +498,7 @@ def run_snap(args):
     for _ in range(args.warmup):
         k.snap(xd, yd, ld, out=out, counts=cnt)
     torch.cuda.synchronize()
-    launches0 = kstats()["kernel_launches"]
+    launches0 = k.stats()["kernel_launches"]
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     with ClockSampler(0) as clk:
@@ -508,7 +508,7 @@ def run_snap(args):
             k.snap(xd, yd, ld, out=out, counts=cnt)
             ev[i][1].record(stream)
         torch.cuda.synchronize()
-    launches = kstats()["kernel_launches"] - launches0
+    launches = k.stats()["kernel_launches"] - launches0
     ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
     # e2e: host inputs (pinned), the Eq. 7 matrix read back every step
     xh, yh, lh = (torch.from_numpy(a).pin_memory() for a in (cloud.x, cloud.y, lab))

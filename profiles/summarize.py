@@ -49,21 +49,27 @@ def launches(path):
     h = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
     hdr = rows[h]
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
-    agg = defaultdict(lambda: [0, 0.0])
-    unit = "ns"
+    mi = hdr.index("Metric Name") if "Metric Name" in hdr else None
+    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+    bscale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}
+    agg = defaultdict(lambda: [0, 0.0, 0.0])  # launches, total us, total dram MB
     for r in rows[h + 1:]:
         if len(r) <= vi:
             continue
-        unit = r[ui]
         name = r[ki].split("(")[0]
-        agg[name][0] += 1
-        agg[name][1] += float(r[vi].replace(",", ""))
+        metric = r[mi] if mi is not None else "gpu__time_duration.sum"
+        v = float(r[vi].replace(",", ""))
+        if metric == "gpu__time_duration.sum":
+            agg[name][0] += 1
+            agg[name][1] += v * scale.get(r[ui], 1e-3)
+        elif metric.startswith("dram__bytes"):
+            agg[name][2] += v * bscale.get(r[ui], 1e-6)
     tot = sum(v[1] for v in agg.values())
     print(f"# {os.path.basename(path)}: {sum(v[0] for v in agg.values())} launches, "
-          f"total {tot / 1e3:.1f} us ({unit} per launch below; cold-cache, serialised)")
-    print(f"{'share':>7} {'count':>6} {'mean_us':>10}  kernel")
+          f"total {tot:.1f} us (cold-cache, serialised; the SHARE is what compares with bench.py)")
+    print(f"{'share':>7} {'count':>6} {'mean_us':>10} {'dram_MB':>9}  kernel")
     for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
-        print(f"{v[1] / tot * 100:6.2f}% {v[0]:6d} {v[1] / v[0] / 1e3:10.2f}  {k}")
+        print(f"{v[1] / tot * 100:6.2f}% {v[0]:6d} {v[1] / v[0]:10.2f} {v[2] / max(v[0], 1):9.1f}  {k}")
 
 
 def report(rep):
@@ -86,9 +92,12 @@ def report(rep):
         print()
 
 
-def traffic(rep, key):
+def traffic(rep, kernel, key=None):
+    """dram bytes per launch of `kernel` (first launch in the report) -> traffic.json[key]
+    (key: "<workload>/<path>/<kernel>", as bench.py looks it up)."""
+    key = key or kernel
     recs, units = _raw(rep)
-    d = [r for r in recs if key in r.get("Kernel Name", "")][0]  # first launch of that kernel
+    d = [r for r in recs if kernel in r.get("Kernel Name", "")][0]
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     b = 0.0
     for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
@@ -102,4 +111,4 @@ def traffic(rep, key):
 
 if __name__ == "__main__":
     {"launches": lambda: launches(sys.argv[2]), "report": lambda: report(sys.argv[2]),
-     "traffic": lambda: traffic(sys.argv[2], sys.argv[3])}[sys.argv[1]]()
+     "traffic": lambda: traffic(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else None)}[sys.argv[1]]()
