@@ -66,7 +66,7 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
 // ---------------------------------------------------------------------------------
 // a2 constants (the convert kernel below already works in sort tiles)
 constexpr int kRsThreads = 256;
-constexpr int kRsMaxBits = 11;
+constexpr int kRsMaxBits = 10;  // (11-bit digits need 8192-key tiles in registers: slower at C5)
 // A sort tile is kRsThreads x rounds keys, rounds = max(8, nbins / 64) rounded up to a
 // power of two: tiles hold at least 4 keys per digit, so the per-tile histograms stay <= 1/4
 // of the keys.
