@@ -24,7 +24,7 @@ inline int seg_pts_for(int64_t n) {
     while (seg < kSegMax && 3 * (int64_t)(2 * seg) <= 2 * (n / kSegShareCtas)) seg *= 2;
     return seg;
 }
-constexpr int kPartPtsDirect = 128;  // direct path: remainder piece = one warp's work item
+constexpr int kPartPtsDirect = 128;  // direct path: smallest remainder piece (one warp's work item)
 constexpr int kCombTile = 32;     // combine-pass output tile edge
 constexpr int kTcM = 128;         // tensor-core tile rows = TMEM lanes
 
