@@ -124,14 +124,14 @@ static int alloc_plan(EvalPlan& pl, const Geom& g) {
 // trip -- unless the splat bound exceeds the context's budget (very large windows): then
 // the exact slot count is read back once and only that much is allocated.
 static int plan_path(kde_ctx* c, EvalPlan& pl, cudaStream_t s) {
-    pl.pg.seg_pts = seg_pts_for(c->stats.n_in);  // global n: identical on every rank
+    pl.pg.seg_pts = seg_pts_for(c->plan_n);  // global n: identical on every rank
     // direct path: remainder pieces of a quarter segment (>= 128 points): fewer splat slots
     // to write, reduce and combine (C4: 128 -> 1024-point pieces, step 2.80 -> 2.62 ms;
     // C2: 128 -> 256, 0.377 -> 0.368 ms).  KDE_PART_PTS overrides (A/B experiments).
     static const int env_part = getenv("KDE_PART_PTS") ? atoi(getenv("KDE_PART_PTS")) : 0;
     const int part = env_part >= 16 ? env_part : std::max(kPartPtsDirect, pl.pg.seg_pts / 4);
     pl.pg.part_pts = pl.part_fixed ? std::min(part, pl.pg.seg_pts) : pl.pg.seg_pts;
-    const int64_t bound = slot_bound(pl.pg, c->stats.n_in);
+    const int64_t bound = slot_bound(pl.pg, std::max(c->stats.n_in, c->plan_n));
     if (bound + 1 > pl.items_cap) {
         if (dalloc((void**)&pl.d_items, sizeof(int4) * (bound + 1), "plan items")) return KDE_ENOMEM;
         pl.items_cap = bound + 1;
@@ -408,6 +408,7 @@ int kde_load_points(kde_ctx* c, const double* x, const double* y, int64_t n) {
     // the previous evaluation reads the sorted points and the plan that binning rewrites
     if (c->evaluated) cudaStreamWaitEvent(c->stream, c->evald_ev, 0);
     tmark(c, 0, c->stream);
+    c->plan_n = n;  // (a banded load replaces it with n_finite)
     int rc = bin_points(c, dx, dy, n);
     if (rc) return rc;
     if (stage_used >= 0) cudaEventRecord(c->stage_free[stage_used], c->stream);

@@ -542,9 +542,12 @@ int bin_points(kde_ctx* c, const double* d_x, const double* d_y, int64_t n64) {
     c->launches += 3;
     uint32_t m = 0;  // the kept count sizes the sort: one readback per banded load
     cudaError_t e = cudaMemcpyAsync(c->h_totals + 28, pb.scan_tmp, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(c->h_totals + 30, pb.nfin, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return cuda_fail(e, "band compaction");
     m = (uint32_t)c->h_totals[28];
+    c->plan_n = (int64_t)*reinterpret_cast<const unsigned long long*>(c->h_totals + 30);
     const int rc = bin_sorted(c, pb.cx, pb.cy, (int)m);  // sorts compacted positions (cidx: originals)
     if (rc) return rc;
     band_stats_kernel<<<1, 1, 0, s>>>(c->d_stats, pb.nfin, c->d_offsets + (size_t)g.nbx * g.nby);

@@ -176,6 +176,9 @@ struct kde_ctx {
     kde_stats stats{};
     bool loaded = false;
     int64_t load_gen = 0;                      // bumped by every load (lazy per-path plans)
+    int64_t plan_n = 0;                        // the point count that sizes the plan's segments:
+                                               // n_in, or n_finite after a banded load (so a
+                                               // NaN-padded point shard plans like the raw set)
     int64_t launches = 0;                      // kernels launched (kde_stats.kernel_launches)
     bool timing = false;                       // record phase events (kde_set_timing)
     cudaEvent_t tev[6] = {};                   // bin0, bin1 (load); plan0, main0, main1, comb1 (eval)
