@@ -183,3 +183,35 @@ def test_O9_dp_properties():
     assert oracle.dp_compress(x, y, offs, 0.0).all()                # eps = 0 keeps noisy data
     col = oracle.dp_compress(np.arange(5.0), 2 * np.arange(5.0), [0, 5], 0.5)
     assert col.tolist() == [1, 0, 0, 0, 1]                          # collinear -> endpoints
+
+
+@pytest.mark.parametrize("stack", [1, 4])
+def test_O8_band_filter_semantics(stack):
+    """The band filter pinned by what it is FOR, not by its formula: (1) completeness -- every
+    finite point whose support (|j + 1/2 - v| <= R, derived here in numpy) reaches a band row
+    and the raster's columns is kept; (2) locality -- a kept point's home row is within the
+    reach plus one stack of the band; (3) the band's density from the kept points alone
+    (renormalised by n) equals the density from all points."""
+    g = _grid(W=64, H=256, hpx=3.0)
+    x, y = _points(g, 3000, 7 + stack)
+    rb, re = 100, 180
+    gb = _grid(W=64, H=256, hpx=3.0, rb=rb, re=re)
+    b = oracle.bin_points(gb, 16, x, y, stack=stack)
+    kept = set(b["perm"].tolist())
+    fin = np.isfinite(x) & np.isfinite(y)
+    u = (x - g.x0) / g.res
+    v = (y - g.y0) / g.res
+    R = oracle.r_px(g)
+    jj = np.arange(rb, re) + 0.5
+    ii = np.arange(g.width) + 0.5
+    for q in np.flatnonzero(fin):
+        reaches = np.any(np.abs(jj - v[q]) <= R) and np.any(np.abs(ii - u[q]) <= R)
+        if reaches:
+            assert q in kept, q                           # (1) completeness
+    hy = np.clip(np.floor(v[list(kept)]), 0, g.height - 1)
+    reach = oracle.reach_px(g)
+    assert np.all(hy >= rb - reach - 16 * stack - 16) and np.all(hy <= re - 1 + reach + 16 * stack + 16)  # (2)
+    sel = np.array(sorted(kept), dtype=np.int64)
+    full, nf = oracle.kde_raster(gb, x, y)
+    part, nk = oracle.kde_raster(gb, x[sel], y[sel])
+    np.testing.assert_allclose(part * (nk / nf), full, rtol=1e-12, atol=1e-300)  # (3)
