@@ -3,7 +3,7 @@
  * estimate of arxiv 2004.13653's visualisation hot path.
  *
  * Citations: P:n = PAPER.md line n (the paper's LaTeX source).
- * §2 restates the operation; DESIGN.md §5 lists the readings (R1..R20).
+ * §2 restates the operation; DESIGN.md §5 lists the readings (R1..R22).
  *
  * Entry points: kde_create / kde_load_points / kde_eval / kde_get_stats /
  * kde_get_bins / kde_set_timing / kde_get_timing / kde_free (the continuous KDE
@@ -129,7 +129,9 @@ typedef struct {
 } kde_stats;
 
 /*
- * kde_create: validate params, plan (bucket size, tiles), and bind the device.
+ * kde_create: validate params, plan (bucket size, tiles), and bind the device.  The
+ * parameters are the paper's problem statement (a u x v grid over the area, Eq. 7's
+ * kernel window P:167-182, the Table 1 kernel P:150-157) with h explicit (R2).
  * Allocates no point-sized buffers and launches no kernels.
  *   p    [in]  parameters, copied.
  *   out  [out] new context; set to NULL on error.
@@ -141,7 +143,13 @@ typedef struct {
 KDE_API int kde_create(const kde_params* p, kde_ctx** out);
 
 /*
- * kde_load_points: replace the context's point set and bin it (steps a1/a2).
+ * kde_load_points: replace the context's point set and bin it (steps a1/a2: the
+ * projection of every point onto the grid, Eqs. 5-6 P:133-139 / Alg. 3 steps 1-2
+ * P:359-373, here onto the fixed world grid with integer support ranges, R5,
+ * and the counting sort that replaces Alg. 3's atomicAdd).
+ * A banded context (row_begin/row_end set) first compacts, in input order, the points
+ * whose home-bucket row lies within the band's reach, and sorts only those (one 4-byte
+ * readback sizes the sort; n_finite still counts every finite point, R4/R22).
  *   x, y [in] n fp64 coordinates (world units), structure-of-arrays; either
  *             both host pointers (copied to the device through a pinned staging
  *             buffer) or both device pointers on params.device.  Not retained.
@@ -165,7 +173,8 @@ KDE_API int kde_create(const kde_params* p, kde_ctx** out);
 KDE_API int kde_load_points(kde_ctx* c, const double* x, const double* y, int64_t n);
 
 /*
- * kde_eval: evaluate the band's raster (steps a3/a4 + a5) into out.
+ * kde_eval: evaluate the band's raster (steps a3/a4 + a5) into out: Eq. 7's kernel
+ * smoothing as the continuous KDE of DESIGN.md §2, scale 1/(n h_px^2).
  *   path   [in] KDE_PATH_DIRECT or KDE_PATH_TENSOR.
  *   out    [out] device pointer on params.device, (row_end-row_begin)*width fp32
  *                (all H*W when the band is 0,0), caller-owned; fully overwritten.
