@@ -239,8 +239,19 @@ def run_ours(args):
     def points(xa, ya):
         return kdist.gather_points(xa, ya) if ws > 1 else (xa, ya)
 
+    peer = kdist.PeerRaster(H, W, device=local) if (ws > 1 and args.fused) else None
+
     def assemble(o):
+        if peer is not None:  # NEXT-F4: the bands are already in rank 0's raster
+            return peer.complete()
         return kdist.gather_to_root(o, bands, H, W) if ws > 1 else o  # a6: NCCL gather to rank 0
+
+    def evaluate(o):
+        if peer is not None:
+            from paper_2004_13653_b200 import _PATHS, kde_eval_ptr
+            kde_eval_ptr(k.ctx, _PATHS[path], peer.band_ptr(rows[0]), stream.cuda_stream)
+        else:
+            k.eval(path, o[:myrows])
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -252,7 +263,7 @@ def run_ours(args):
         x, y = points(xs, ys)
         if k is not None:
             k.load(x, y)
-            k.eval(path, out[:myrows])
+            evaluate(out)
         return assemble(out)
 
     for _ in range(args.warmup):
@@ -328,7 +339,7 @@ def run_ours(args):
         elif k is not None:
             k.load(xh, yh)  # host buffers straight through the C ABI (H2D inside kde_load_points)
         if k is not None:
-            k.eval(path, o[:myrows])
+            evaluate(o)
         full = assemble(o)
         ready = torch.cuda.Event()
         ready.record(stream)
@@ -440,7 +451,7 @@ def run_ours(args):
                                           if args.dp_eps is not None else None),
                    "cutoff": cfg["cutoff"], "kernel": cfg["kernel"],
                    "form": "radial" if cfg["radial"] else "product",
-                   "parallelism": f"row-bands x{ws}" if ws > 1 else "single",
+                   "parallelism": (f"row-bands x{ws}" + (" fused-peer" if args.fused else "")) if ws > 1 else "single",
                    "bands": bands if ws > 1 else None,
                    "l2": "flushed (512 MiB write) before every timed step"},
         "pixels_per_s": W * H / (ms * 1e-3),
@@ -660,6 +671,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--fused", action="store_true",
+                    help="N > 1: bands written into rank 0's raster through peer memory (NEXT-F4) "
+                         "instead of the NCCL gather")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(_spawn(args))

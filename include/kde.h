@@ -283,6 +283,25 @@ KDE_API int kde_snap(kde_ctx* c, const double* x, const double* y, const int32_t
 KDE_API int kde_dp(const double* x, const double* y, const int64_t* traj_offsets, int64_t ntraj, double eps,
                    uint8_t* keep, int32_t device, void* stream, int64_t* n_kept, int64_t* rounds);
 
+/*
+ * Peer-memory band assembly (NEXT-F4): rank 0 exports its H x W raster, every
+ * other rank maps it and passes (mapped pointer + row_begin * width) as kde_eval's `out`, so
+ * the combine kernel's epilogue stores the band straight into rank 0's memory -- over NVLink
+ * P2P between GPUs (no separate gather), through the same device's memory in the one-GPU
+ * tests.  The paper's SR counts every transfer; this removes the gather's.
+ *   kde_ipc_export: handle [out] 64 bytes (cudaIpcMemHandle_t) of the allocation holding
+ *                   dev_ptr [in] (a device pointer from cudaMalloc, e.g. a torch tensor's
+ *                   storage); *offset [out] = dev_ptr minus the allocation's base.
+ *   kde_ipc_open:   map another process's exported allocation on `device`; *dev_ptr [out]
+ *                   = its base (add the exporter's offset).  Close with kde_ipc_close.
+ * Synchronisation is the caller's: the exporter must not read the raster before every
+ * writer's eval stream has completed (e.g. stream synchronise + a process-group barrier).
+ * Errors: KDE_EINVAL (NULL), KDE_ECUDA.
+ */
+KDE_API int kde_ipc_export(const void* dev_ptr, void* handle, int64_t* offset);
+KDE_API int kde_ipc_open(const void* handle, int32_t device, void** dev_ptr);
+KDE_API int kde_ipc_close(void* dev_ptr, int32_t device);
+
 /* Thread-local message describing the last non-OK return on this thread. */
 KDE_API const char* kde_last_error(void);
 

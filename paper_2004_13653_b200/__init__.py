@@ -17,11 +17,12 @@ from ._lib import (KDE_COSINE, KDE_EPANECHNIKOV, KDE_GAUSSIAN, KDE_PATH_DIRECT,
                    KDE_PATH_TENSOR, KDE_PATH_TENSOR_SPLIT, KDE_QUARTIC, KDE_RADIAL, KDE_TRIANGULAR, KDE_TRICUBE,
                    KDE_TRIWEIGHT, KDE_UNIFORM, KERNEL_NAMES, KdeError, kde_create, kde_eval,
                    kde_free, kde_get_bins, kde_get_stats, kde_get_timing, kde_last_error,
-                   kde_load_points, kde_params, kde_set_timing, kde_snap, kde_dp)
+                   kde_load_points, kde_params, kde_set_timing, kde_snap, kde_dp,
+                   kde_eval_ptr, kde_ipc_close, kde_ipc_export, kde_ipc_open)
 
 __all__ = ["KDE", "KdeError", "kde_params", "kde_create", "kde_load_points", "kde_eval",
            "kde_get_stats", "kde_get_bins", "kde_set_timing", "kde_get_timing", "kde_snap", "kde_dp", "kde_last_error",
-           "kde_free", "KERNEL_NAMES",
+           "kde_free", "kde_eval_ptr", "kde_ipc_export", "kde_ipc_open", "kde_ipc_close", "KERNEL_NAMES",
            "KDE_PATH_DIRECT", "KDE_PATH_TENSOR", "KDE_PATH_TENSOR_SPLIT", "KDE_RADIAL", "kernel_id"]
 
 

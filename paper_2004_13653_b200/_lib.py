@@ -26,7 +26,8 @@ _CODES = {KDE_EINVAL: "EINVAL", KDE_ENOMEM: "ENOMEM", KDE_ECUDA: "ECUDA",
           KDE_EUNSUPPORTED: "EUNSUPPORTED", KDE_ESTATE: "ESTATE"}
 
 EXPORTS = ("kde_create", "kde_load_points", "kde_eval", "kde_get_stats", "kde_get_bins",
-           "kde_set_timing", "kde_get_timing", "kde_snap", "kde_dp", "kde_last_error", "kde_free")
+           "kde_set_timing", "kde_get_timing", "kde_snap", "kde_dp", "kde_ipc_export", "kde_ipc_open",
+           "kde_ipc_close", "kde_last_error", "kde_free")
 
 
 class kde_params(ctypes.Structure):
@@ -79,10 +80,14 @@ def _load():
     L.kde_snap.argtypes = [vp, vp, vp, vp, ctypes.c_int64, vp, vp, vp]
     L.kde_dp.argtypes = [vp, vp, vp, ctypes.c_int64, ctypes.c_double, vp, ctypes.c_int32, vp,
                          P(ctypes.c_int64), P(ctypes.c_int64)]
+    L.kde_ipc_export.argtypes = [vp, vp, P(ctypes.c_int64)]
+    L.kde_ipc_open.argtypes = [vp, ctypes.c_int32, P(vp)]
+    L.kde_ipc_close.argtypes = [vp, ctypes.c_int32]
     L.kde_free.argtypes = [vp]
     L.kde_free.restype = None
     for f in ("kde_create", "kde_load_points", "kde_eval", "kde_get_stats", "kde_get_bins",
-              "kde_set_timing", "kde_get_timing", "kde_snap", "kde_dp"):
+              "kde_set_timing", "kde_get_timing", "kde_snap", "kde_dp", "kde_ipc_export", "kde_ipc_open",
+              "kde_ipc_close"):
         getattr(L, f).restype = ctypes.c_int
     return L
 
@@ -160,6 +165,12 @@ def kde_eval(ctx: int, path: int, out, stream: int | None = None) -> None:
         import torch
         stream = torch.cuda.current_stream(out.device).cuda_stream
     _check(_L.kde_eval(ctx, int(path), _ptr(out), stream))
+
+
+def kde_eval_ptr(ctx: int, path: int, out_ptr: int, stream: int) -> None:
+    """kde_eval into a raw device pointer (e.g. a peer's raster mapped with kde_ipc_open, at
+    the band's first row): the caller guarantees (row_end-row_begin)*W fp32 behind it."""
+    _check(_L.kde_eval(ctx, int(path), ctypes.c_void_p(out_ptr), stream))
 
 
 def kde_snap(ctx: int, x, y, label, out, counts=None, stream: int | None = None) -> None:
@@ -250,6 +261,27 @@ def kde_get_timing(ctx: int) -> dict:
     t = kde_timing()
     _check(_L.kde_get_timing(ctx, ctypes.byref(t)))
     return {f: float(getattr(t, f)) for f, _ in t._fields_}
+
+
+def kde_ipc_export(dev_ptr: int):
+    """(64-byte handle, byte offset) of the device allocation holding dev_ptr."""
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_int64(0)
+    _check(_L.kde_ipc_export(ctypes.c_void_p(dev_ptr), h, ctypes.byref(off)))
+    return h.raw, off.value
+
+
+def kde_ipc_open(handle: bytes, device: int) -> int:
+    """Map another process's exported allocation; returns its base device pointer."""
+    if len(handle) != 64:
+        raise ValueError("an IPC handle is 64 bytes")
+    p = ctypes.c_void_p()
+    _check(_L.kde_ipc_open(ctypes.create_string_buffer(handle, 64), int(device), ctypes.byref(p)))
+    return p.value
+
+
+def kde_ipc_close(dev_ptr: int, device: int) -> None:
+    _check(_L.kde_ipc_close(ctypes.c_void_p(dev_ptr), int(device)))
 
 
 def kde_free(ctx: int | None) -> None:

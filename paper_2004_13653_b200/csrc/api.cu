@@ -9,6 +9,8 @@
 #include <algorithm>
 #include <numeric>
 
+#include <dlfcn.h>
+
 #include "internal.cuh"
 
 namespace kde {
@@ -725,6 +727,65 @@ int kde_dp(const double* x, const double* y, const int64_t* traj_offsets, int64_
     cudaFree(doff);
     cudaFree(dk);
     return rc;
+}
+
+int kde_ipc_export(const void* dev_ptr, void* handle, int64_t* offset) {
+    if (!dev_ptr || !handle || !offset) {
+        set_error("kde_ipc_export: NULL argument");
+        return KDE_EINVAL;
+    }
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, dev_ptr) != cudaSuccess || at.type != cudaMemoryTypeDevice) {
+        cudaGetLastError();
+        set_error("kde_ipc_export: not a device pointer");
+        return KDE_EINVAL;
+    }
+    DeviceGuard dg(at.device);
+    // the allocation's base (IPC handles name whole allocations; a torch tensor may sit inside
+    // a larger cached block): the driver's cuMemGetAddressRange, looked up at run time so the
+    // library keeps no link-time dependency on libcuda (CPU-only hosts still load it)
+    using GetRange = int (*)(unsigned long long*, size_t*, unsigned long long);
+    void* drv = dlopen("libcuda.so.1", RTLD_NOW | RTLD_NOLOAD);
+    if (!drv) drv = dlopen("libcuda.so.1", RTLD_NOW);
+    GetRange get_range = drv ? reinterpret_cast<GetRange>(dlsym(drv, "cuMemGetAddressRange_v2")) : nullptr;
+    unsigned long long base_u = 0;
+    size_t size = 0;
+    if (!get_range || get_range(&base_u, &size, (unsigned long long)(uintptr_t)dev_ptr) != 0) {
+        set_error("kde_ipc_export: cuMemGetAddressRange unavailable or failed");
+        return KDE_ECUDA;
+    }
+    void* base = reinterpret_cast<void*>((uintptr_t)base_u);
+    cudaIpcMemHandle_t h;
+    const cudaError_t e = cudaIpcGetMemHandle(&h, base);
+    if (e != cudaSuccess) return cuda_fail(e, "kde_ipc_export");
+    memcpy(handle, &h, sizeof h);
+    *offset = (int64_t)((const char*)dev_ptr - (const char*)base);
+    return KDE_OK;
+}
+
+int kde_ipc_open(const void* handle, int32_t device, void** dev_ptr) {
+    if (!handle || !dev_ptr) {
+        set_error("kde_ipc_open: NULL argument");
+        return KDE_EINVAL;
+    }
+    DeviceGuard dg(device);
+    if (!dg.ok) return cuda_fail(cudaGetLastError(), "kde_ipc_open: cudaSetDevice");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof h);
+    const cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail(e, "kde_ipc_open");
+    return KDE_OK;
+}
+
+int kde_ipc_close(void* dev_ptr, int32_t device) {
+    if (!dev_ptr) {
+        set_error("kde_ipc_close: NULL argument");
+        return KDE_EINVAL;
+    }
+    DeviceGuard dg(device);
+    const cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+    if (e != cudaSuccess) return cuda_fail(e, "kde_ipc_close");
+    return KDE_OK;
 }
 
 void kde_free(kde_ctx* c) {

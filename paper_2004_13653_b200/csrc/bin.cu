@@ -618,7 +618,6 @@ static int bin_sorted(kde_ctx* c, const double* d_x, const double* d_y, int n) {
     }
     cudaMemsetAsync(c->d_stats, 0, 3 * sizeof(unsigned long long), s);
     if (n > 0) {
-        const size_t up_smem = sizeof(uint32_t) * nbins;
         // small digit sets scatter short runs: stage the tile digit-sorted in shared memory
         // and write it out coalesced; large ones scatter directly
         auto dn_smem = [&](int nbp, bool stg) {

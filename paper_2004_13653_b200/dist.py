@@ -163,6 +163,63 @@ def gather_to_root(band, rows, H, W, group=None, root: int = 0):
     return None
 
 
+class PeerRaster:
+    """NEXT-F4, fused band assembly: rank 0's (H, W) raster mapped into every rank's address
+    space (CUDA IPC through libkde: kde_ipc_export / kde_ipc_open; over NVLink P2P between
+    GPUs), so each rank's kde_eval writes its band straight into rank 0's memory from the
+    combine kernel's epilogue -- no separate gather.  ``complete()``: stream sync + barrier,
+    after which rank 0's ``full`` holds the whole raster."""
+
+    def __init__(self, H, W, device=0, group=None):
+        import torch
+        import torch.distributed as dist
+
+        from . import kde_ipc_export, kde_ipc_open
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.H, self.W, self.device = int(H), int(W), int(device)
+        dev = torch.device("cuda", self.device)
+        payload = torch.zeros(72, dtype=torch.uint8)
+        self.full = None
+        if self.rank == 0:
+            self.full = torch.zeros((self.H, self.W), dtype=torch.float32, device=dev)
+            handle, off = kde_ipc_export(self.full.data_ptr())
+            payload[:64] = torch.frombuffer(bytearray(handle), dtype=torch.uint8)
+            payload[64:] = torch.frombuffer(bytearray(int(off).to_bytes(8, "little", signed=True)),
+                                            dtype=torch.uint8)
+        if dist.get_backend(group) == "nccl":
+            pd = payload.to(dev)
+            dist.broadcast(pd, src=0, group=group)
+            payload = pd.cpu()
+        else:
+            dist.broadcast(payload, src=0, group=group)
+        raw = bytes(payload.tolist())
+        off = int.from_bytes(raw[64:], "little", signed=True)
+        self._mapped = None
+        if self.rank == 0:
+            self.base = self.full.data_ptr()
+        else:
+            self._mapped = kde_ipc_open(raw[:64], self.device)
+            self.base = self._mapped + off
+
+    def band_ptr(self, rb):
+        """Device address of row rb of rank 0's raster (kde_eval_ptr's `out`)."""
+        return self.base + 4 * rb * self.W
+
+    def complete(self):
+        import torch
+        import torch.distributed as dist
+        torch.cuda.current_stream(torch.device("cuda", self.device)).synchronize()
+        dist.barrier(group=self.group)
+        return self.full
+
+    def close(self):
+        from . import kde_ipc_close
+        if self._mapped:
+            kde_ipc_close(self._mapped, self.device)
+            self._mapped = None
+
+
 class ShardedKDE:
     """A KDE whose raster is split in row bands over the ranks of a process group.
 
@@ -213,8 +270,19 @@ class ShardedKDE:
             self.kde.load(x, y)
         return self
 
-    def eval(self, path="direct", everywhere=False):
+    def eval(self, path="direct", everywhere=False, peer: "PeerRaster | None" = None):
+        """The full raster on rank 0 (None elsewhere): gathered over the process group, or --
+        with `peer` (NEXT-F4) -- written by every rank's combine straight into rank 0's
+        memory."""
         import torch
+        if peer is not None:
+            from . import _PATHS, kde_eval_ptr
+            if self.kde is not None:
+                rb, _ = self.rows[self.rank]
+                p = _PATHS[path] if isinstance(path, str) else int(path)
+                stream = torch.cuda.current_stream(torch.device("cuda", self.device)).cuda_stream
+                kde_eval_ptr(self.kde.ctx, p, peer.band_ptr(rb), stream)
+            return peer.complete()
         maxr = max(re - rb for rb, re in self.rows)
         band = torch.zeros((maxr, self.W), dtype=torch.float32, device=torch.device("cuda", self.device))
         if self.kde is not None:

@@ -18,7 +18,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 from paper_2004_13653_b200 import KDE  # noqa: E402
-from paper_2004_13653_b200.dist import ShardedKDE, shard_points  # noqa: E402
+from paper_2004_13653_b200.dist import PeerRaster, ShardedKDE, shard_points  # noqa: E402
 from tests.gpu_cases import case  # noqa: E402
 
 
@@ -38,11 +38,16 @@ def main():
         sk.load(xs, ys)
         full = sk.eval(path)
         full = full.cpu().numpy() if full is not None else None
+        peer = PeerRaster(c["H"], c["W"], device=dev)  # NEXT-F4: bands written into rank 0's raster
+        fused = sk.eval(path, peer=peer)
+        fused = fused.cpu().numpy() if fused is not None else None
+        peer.close()
         if rank == 0:
             ref = KDE(c["x0"], c["y0"], c["res"], c["W"], c["H"], c["h"], device=dev)
             ref.load(torch.from_numpy(c["x"]).cuda(dev), torch.from_numpy(c["y"]).cuda(dev))
             r = ref.eval(path).cpu().numpy()
             res[path] = bool(np.array_equal(full.view(np.uint32), r.view(np.uint32)))
+            res[path + "_fused"] = bool(np.array_equal(fused.view(np.uint32), r.view(np.uint32)))
             res["bands"] = sk.rows
             res["n_finite"] = sk.kde.stats()["n_finite"] == ref.stats()["n_finite"]
     if rank == 0:
