@@ -447,7 +447,11 @@ int launch_tc(kde_ctx* c, float* out, cudaStream_t s, bool split) {
         {launch_tc_h<1, 0, true, true>, launch_tc_h<1, 1, true, true>, launch_tc_h<1, 2, true, true>,
          launch_tc_h<1, 3, true, true>, launch_tc_h<1, 4, true, true>, launch_tc_h<1, 5, true, true>,
          launch_tc_h<1, 6, true, true>, launch_tc_h<1, 7, true, true>}};
-    if (c->kern == KDE_GAUSSIAN && !rec)
+    const int rc5 = split ? KDE_EUNSUPPORTED : launch_tc5(c, s);  // eval_tc5.cu when it applies
+    if (rc5 != KDE_OK && rc5 != KDE_EUNSUPPORTED) return rc5;
+    if (rc5 == KDE_OK)
+        ;
+    else if (c->kern == KDE_GAUSSIAN && !rec)
         (split ? launch_tc_h<1, 6, true, false> : launch_tc_h<1, 6, false, false>)(c, pl, a, s);
     else
         kLaunch[split ? 1 : 0][c->kern](c, pl, a, s);

@@ -200,6 +200,7 @@ int bin_points(kde_ctx* c, const double* d_x, const double* d_y, int64_t n);
 // evaluation (eval_direct.cu, eval_tc.cu)
 int launch_direct(kde_ctx* c, float* out, cudaStream_t s);
 int launch_tc(kde_ctx* c, float* out, cudaStream_t s, bool split);
+int launch_tc5(kde_ctx* c, cudaStream_t s);  // eval_tc5.cu: per-warp tensor-core pipelines
 // planning (plan.cu)
 int plan_device(kde_ctx* c, EvalPlan& pl, cudaStream_t s);
 int plan_nblk(const PathGeom& pg);
