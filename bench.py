@@ -422,17 +422,17 @@ def run_ours(args):
         peak = peaks["bf16_tflops"]
         mma = st["tc_mma_flops"] * (3 if path == "tensor_split" else 1)  # split: 3 MMAs / K step
         useful_tf = 2.0 * st["useful_pairs"] / (eval_ms * 1e-3) / 1e12
-        roof = {"bound": "tensor", "kernel": "tc_splat_kernel",
+        roof = {"bound": "tensor", "kernel": {3: "tc5_kernel"}.get(st.get("main_kernel"), "tc_splat_kernel"),
                 "achieved": useful_tf,
                 "peak": peak, "unit": "TFLOP/s",
                 "peak_source": f"{peak_src} bf16_tflops (fp16 dense rate = bf16)",
                 "achieved_counts": "2 flops per useful pair (kde_stats.useful_pairs)",
                 "executed_mma_flops_per_launch": mma,
                 "executed_mma_tflops": round(mma / (eval_ms * 1e-3) / 1e12, 3),
-                "executed_frac": round(mma / (eval_ms * 1e-3) / 1e12 / peak, 4),
+                "executed_frac": float(f"{mma / (eval_ms * 1e-3) / 1e12 / peak:.4g}"),
                 "useful_share_of_mma": round(2.0 * st["useful_pairs"] / max(mma, 1), 4)}
-    roof["achieved"] = round(roof["achieved"], 3)
-    roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
+    roof["frac"] = float(f"{roof['achieved'] / roof['peak']:.4g}")
+    roof["achieved"] = float(f"{roof['achieved']:.6g}")
     roof["traffic"] = _traffic(f"{_workload_key(args)}/{path}/{roof['kernel']}")
     roof["traffic_key"] = f"{_workload_key(args)}/{path}/{roof['kernel']}"
     roof["kernel_ms"] = round(eval_ms, 4)

@@ -126,6 +126,10 @@ typedef struct {
     int64_t tc_mma_flops;  /* tensor-core flops one KDE_PATH_TENSOR eval of the last load
                               executes (2 per MMA multiply-add; 0 until that path has been
                               evaluated for the load): the tensor-pipe roofline numerator   */
+    int32_t main_kernel;   /* the main (a3/a4) kernel of the last kde_eval: 0 none yet,
+                              1 splat_kernel (direct), 2 tc_splat_kernel (tensor, eval_tc.cu),
+                              3 tc5_kernel (tensor, per-warp pipelines, eval_tc5.cu)         */
+    int32_t reserved;      /* 0                                                              */
 } kde_stats;
 
 /*

@@ -520,15 +520,20 @@ int kde_get_stats(const kde_ctx* c, kde_stats* s) {
     if (rc) return rc;
     *s = c->stats;
     s->kernel_launches = c->launches;
+    s->main_kernel = c->main_kernel;
+    s->reserved = 0;
     s->tc_mma_flops = 0;
     const EvalPlan& tp = c->plan[KDE_PATH_TENSOR];
     if (c->loaded && tp.enabled && tp.planned_gen == c->load_gen) {  // executed MMA flops / eval
-        int chunks = 0;
+        int tot[kTotInts] = {};
         // the plan was built on the eval's (possibly non-blocking) stream: wait for that
         // eval before reading its totals
         cudaError_t e = c->evaluated ? cudaEventSynchronize(c->evald_ev) : cudaSuccess;
-        if (e == cudaSuccess) e = cudaMemcpy(&chunks, tp.d_totals + kTotChunks, sizeof(int), cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess) e = cudaMemcpy(tot, tp.d_totals, sizeof(tot), cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) return cuda_fail(e, "kde_get_stats");
+        // the per-warp kernel (eval_tc5.cu) counts the chunks it executed; the other kernel
+        // executes the plan's chunks
+        const int chunks = tot[kTotChunksExec] > 0 ? tot[kTotChunksExec] : tot[kTotChunks];
         // per chunk: chunk_pts/16 MMAs of M=128 x N x K=16, 2 flops per MAC
         s->tc_mma_flops = (int64_t)chunks * (tp.pg.chunk_pts / 16) * 2 * kTcM * tp.pg.mma_n * 16;
     }
@@ -805,6 +810,8 @@ void kde_free(kde_ctx* c) {
         cudaFree(pb.val[k]);
     }
     cudaFree(pb.hist);
+    cudaFree(pb.ost[0]);
+    cudaFree(pb.ost[1]);
     cudaFree(pb.scan_tmp);
     cudaFree(pb.rec);
     cudaFree(pb.xy);

@@ -22,6 +22,15 @@ struct Binned {
     float lx, ly;
 };
 
+// fp64 floor / ceil to int by the round-to-integer of an add to 1.5 * 2^52 (ulp 1 there):
+// exact for |a| < 2^31, on the FP64 pipe instead of the XU pipe's F2I/FRND.
+__device__ __forceinline__ int dfloor_i(double a) {
+    return (int)(uint32_t)__double_as_longlong(__dadd_rd(a, 6755399441055744.0));
+}
+__device__ __forceinline__ int dceil_i(double a) {
+    return (int)(uint32_t)__double_as_longlong(__dadd_ru(a, 6755399441055744.0));
+}
+
 __device__ __forceinline__ Binned bin_point(double x, double y, const Geom& g, uint32_t sentinel) {
     Binned b;
     b.key = sentinel;
@@ -32,26 +41,39 @@ __device__ __forceinline__ Binned bin_point(double x, double y, const Geom& g, u
     b.status = 1;
     const double u = __ddiv_rn(__dsub_rn(x, g.x0), g.res);
     const double v = __ddiv_rn(__dsub_rn(y, g.y0), g.res);
-    double ilo = ceil(__dsub_rn(__dsub_rn(u, 0.5), g.R));
-    double ihi = floor(__dadd_rn(__dsub_rn(u, 0.5), g.R));
-    double jlo = ceil(__dsub_rn(__dsub_rn(v, 0.5), g.R));
-    double jhi = floor(__dadd_rn(__dsub_rn(v, 0.5), g.R));
-    ilo = fmax(ilo, 0.0);
-    ihi = fmin(ihi, (double)(g.W - 1));
-    jlo = fmax(jlo, 0.0);
-    jhi = fmin(jhi, (double)(g.H - 1));
-    if (ilo > ihi || jlo > jhi) return b;  // window misses the raster
-    const double fu = floor(u), fv = floor(v);
-    const int hx = fu < 0.0 ? 0 : (fu > (double)(g.W - 1) ? g.W - 1 : (int)fu);
-    const int hy = fv < 0.0 ? 0 : (fv > (double)(g.H - 1) ? g.H - 1 : (int)fv);
+    const double ilo_a = __dsub_rn(__dsub_rn(u, 0.5), g.R), ihi_a = __dadd_rn(__dsub_rn(u, 0.5), g.R);
+    const double jlo_a = __dsub_rn(__dsub_rn(v, 0.5), g.R), jhi_a = __dadd_rn(__dsub_rn(v, 0.5), g.R);
+    int ilo, ihi, jlo, jhi, hx, hy;
+    if (fabs(u) + g.R < 1073741824.0 && fabs(v) + g.R < 1073741824.0) {
+        // |every rounded value| < 2^31: integer floor/ceil by the add-to-1.5*2^52 rounding
+        // (the same values as ceil/floor of the same fp64 operands), clamps in integers
+        ilo = max(dceil_i(ilo_a), 0);
+        ihi = min(dfloor_i(ihi_a), g.W - 1);
+        jlo = max(dceil_i(jlo_a), 0);
+        jhi = min(dfloor_i(jhi_a), g.H - 1);
+        if (ilo > ihi || jlo > jhi) return b;  // window misses the raster
+        hx = min(max(dfloor_i(u), 0), g.W - 1);
+        hy = min(max(dfloor_i(v), 0), g.H - 1);
+    } else {  // far outside (or a huge support): the written fp64 formulas
+        const double ilod = fmax(ceil(ilo_a), 0.0), ihid = fmin(floor(ihi_a), (double)(g.W - 1));
+        const double jlod = fmax(ceil(jlo_a), 0.0), jhid = fmin(floor(jhi_a), (double)(g.H - 1));
+        if (ilod > ihid || jlod > jhid) return b;  // window misses the raster
+        ilo = (int)ilod;
+        ihi = (int)ihid;
+        jlo = (int)jlod;
+        jhi = (int)jhid;
+        const double fu = floor(u), fv = floor(v);
+        hx = fu < 0.0 ? 0 : (fu > (double)(g.W - 1) ? g.W - 1 : (int)fu);
+        hy = fv < 0.0 ? 0 : (fv > (double)(g.H - 1) ? g.H - 1 : (int)fv);
+    }
     const int bx = hx >> g.lgB, by = hy >> g.lgB;  // B is a power of two
     if (by < g.band_lo || by > g.band_hi) return b;  // outside the band's reach
     b.status = 2;
     b.key = (uint32_t)(bx * g.nby + by);  // column-major: a vertical bucket stack is contiguous
-    b.ilo = (int)ilo;
-    b.ihi = (int)ihi;
-    b.jlo = (int)jlo;
-    b.jhi = (int)jhi;
+    b.ilo = ilo;
+    b.ihi = ihi;
+    b.jlo = jlo;
+    b.jhi = jhi;
     b.lx = __double2float_rn(__dsub_rn(u, (double)(bx * g.B)));
     b.ly = __double2float_rn(__dsub_rn(v, (double)(by * g.B)));
     return b;
@@ -64,51 +86,70 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
 }
 
 // ---------------------------------------------------------------------------------
-// a2 constants (the convert kernel below already works in sort tiles)
+// a2 constants
 constexpr int kRsThreads = 256;
-constexpr int kRsMaxBits = 10;  // (11-bit digits need 8192-key tiles in registers: slower at C5)
+constexpr int kRsMaxBits = 10;  // digits of <= 10 bits: <= 1025 digits per pass (incl. sentinel)
+constexpr int kRsMaxDigits = 1025;
+constexpr int kRsMaxPasses = 3;   // keys < 2^30
 // A sort tile is kRsThreads x rounds keys, rounds = max(8, nbins / 64) rounded up to a
-// power of two: tiles hold at least 4 keys per digit, so the per-tile histograms stay <= 1/4
-// of the keys.
+// power of two: tiles hold at least 4 keys per digit.
 inline int rs_rounds(int nbins) {
     int r = 8;
     while (r * 64 + 64 < nbins) r *= 2;  // (a last digit set of 2^k + 1 keeps 2^k / 64)
     return r;
 }
 
-// a1 kernel, one sort tile (kRsThreads x rounds points) per CTA: keys, the point's record (bucket-
-// local fp32 coordinates + packed int16 ranges, read back by the gather), the integer
-// stats (n_finite, n_outside, useful_pairs) and the tile's histogram of the first radix
-// digit (the first pass's upsweep, fused).
+// the first tile of radix CTA c's range (os_pass_kernel)
+__host__ __device__ inline int os_tile_begin(int c, int ntiles, int nctas) {
+    return (int)(((int64_t)c * ntiles) / nctas);
+}
+
+// a1 kernel: each CTA converts the contiguous range of whole sort tiles the first radix
+// pass's CTA of the same index sorts.  Keys, the point's
+// record (bucket-local fp32 coordinates + packed int16 ranges, read back by the gather), the
+// integer stats (n_finite, n_outside, useful_pairs), and the GLOBAL histogram of every radix
+// pass's digit (shared-memory counts, one global add per nonzero count per CTA): the
+// radix passes take the digit offsets from these totals; the first pass's range histogram
+// is this CTA's count of its digit.
 __global__ void __launch_bounds__(kRsThreads, 4) bin_convert_kernel(
     const double* __restrict__ x, const double* __restrict__ y, int n, Geom g, uint32_t sentinel,
     uint32_t* __restrict__ key, uint4* __restrict__ rec, unsigned long long* __restrict__ stats,
-    uint32_t dmask, int nbins, uint32_t* __restrict__ hist, int hstride, int rounds) {
-    extern __shared__ uint32_t h[];  // [nbins]
-    for (int d = threadIdx.x; d < nbins; d += kRsThreads) h[d] = 0;
+    int passes, int dbits, uint32_t* __restrict__ ghist, int tile, int ntiles, uint32_t* __restrict__ rowhist0,
+    int nbins0, int split) {
+    __shared__ uint32_t h[kRsMaxPasses * kRsMaxDigits];
+    for (int d = threadIdx.x; d < passes * kRsMaxDigits; d += kRsThreads) h[d] = 0;
     unsigned long long nf = 0, no = 0, up = 0;
     const int rb = g.rb, re = g.re;
-    const int base = blockIdx.x * kRsThreads * rounds + threadIdx.x;
+    const uint32_t lmask = (1u << dbits) - 1u;
+    // part blockIdx.x % split of the range of the first radix pass's CTA blockIdx.x / split
+    // (os_pass_kernel): whole tiles
+    const int pc = blockIdx.x / split, part = blockIdx.x % split, nc = gridDim.x / split;
+    const int tb = os_tile_begin(pc, ntiles, nc), te = os_tile_begin(pc + 1, ntiles, nc);
+    const int beg = (tb + (int)(((int64_t)part * (te - tb)) / split)) * tile;
+    const int end = min(n, (tb + (int)(((int64_t)(part + 1) * (te - tb)) / split)) * tile);
     __syncthreads();
     constexpr int kHalf = 4;  // batches of loads-then-compute
-    for (int hb = 0; hb < rounds / kHalf; hb++) {
+    for (int b0 = beg + threadIdx.x; b0 < end; b0 += kHalf * kRsThreads) {
         double xv[kHalf], yv[kHalf];
 #pragma unroll
         for (int r = 0; r < kHalf; r++) {
-            const int i = base + (hb * kHalf + r) * kRsThreads;
-            xv[r] = i < n ? x[i] : 0.0;
-            yv[r] = i < n ? y[i] : 0.0;
+            const int i = b0 + r * kRsThreads;
+            xv[r] = i < end ? x[i] : 0.0;
+            yv[r] = i < end ? y[i] : 0.0;
         }
 #pragma unroll
         for (int r = 0; r < kHalf; r++) {
-            const int i = base + (hb * kHalf + r) * kRsThreads;
-            if (i >= n) break;
+            const int i = b0 + r * kRsThreads;
+            if (i >= end) break;
             const Binned b = bin_point(xv[r], yv[r], g, sentinel);
             key[i] = b.key;
             rec[i] = make_uint4(__float_as_uint(b.lx), __float_as_uint(b.ly),
                                 ((uint32_t)b.ilo & 0xffffu) | ((uint32_t)b.ihi << 16),
                                 ((uint32_t)b.jlo & 0xffffu) | ((uint32_t)b.jhi << 16));
-            atomicAdd(&h[b.key & dmask], 1u);
+            for (int ps = 0; ps < passes; ps++) {
+                const uint32_t dg = b.key >> (ps * dbits);
+                atomicAdd(&h[ps * kRsMaxDigits + (ps == passes - 1 ? dg : dg & lmask)], 1u);
+            }
             nf += b.status > 0;
             no += b.status == 1;
             if (b.status == 2) {
@@ -133,31 +174,10 @@ __global__ void __launch_bounds__(kRsThreads, 4) bin_convert_kernel(
         for (int k = 0; k < kRsThreads / 32; k++) t += s[threadIdx.x][k];
         if (t) atomicAdd(&stats[threadIdx.x], t);
     }
-    for (int d = threadIdx.x; d < nbins; d += kRsThreads) hist[(size_t)d * hstride + blockIdx.x] = h[d];
-}
-
-// ---------------------------------------------------------------------------------
-// a2: stable LSD counting sort.  Keys lie in [0, nb] (nb = dropped); passes =
-// ceil(bits/10) with digits of ceil(bits/passes) <= 10 bits (two passes up to 2^20
-// buckets, three up to 2^30).  Per pass: per-tile digit histograms (pass 0: fused into
-// the convert kernel) -> per-digit exclusive scan over the tiles + digit totals (one
-// kernel) -> stable in-tile ranking into a digit-sorted shared-memory copy of the tile
-// -> coalesced write-out, each tile adding the exclusive scan of the digit totals.
-
-__global__ void __launch_bounds__(kRsThreads) rs_upsweep(const uint32_t* __restrict__ keys, int n,
-                                                         int shift, uint32_t dmask, int nbins,
-                                                         uint32_t* __restrict__ hist, int hstride, int rounds) {
-    extern __shared__ uint32_t h[];  // [nbins]
-    for (int d = threadIdx.x; d < nbins; d += kRsThreads) h[d] = 0;
-    __syncthreads();
-    const int base = blockIdx.x * kRsThreads * rounds;
-#pragma unroll 8
-    for (int r = 0; r < rounds; r++) {
-        const int i = base + r * kRsThreads + threadIdx.x;
-        if (i < n) atomicAdd(&h[(keys[i] >> shift) & dmask], 1u);
-    }
-    __syncthreads();
-    for (int d = threadIdx.x; d < nbins; d += kRsThreads) hist[(size_t)d * hstride + blockIdx.x] = h[d];
+    for (int d = threadIdx.x; d < passes * kRsMaxDigits; d += kRsThreads)
+        if (h[d]) atomicAdd(&ghist[d], h[d]);
+    for (int d = threadIdx.x; d < nbins0; d += kRsThreads)  // the first pass's range histogram
+        if (h[d]) atomicAdd(&rowhist0[(size_t)pc * nbins0 + d], h[d]);
 }
 
 // exclusive scan of a[0..nb) in shared memory, in place (all kRsThreads threads call it)
@@ -190,108 +210,265 @@ __device__ __forceinline__ void block_scan_smem(uint32_t* a, int nb, uint32_t* s
     __syncthreads();
 }
 
-// Stable scatter of one tile (kRsThreads x ROUNDS keys, ROUNDS = rs_rounds(nbins)).  Warp w
-// owns the contiguous sub-range [w*32*ROUNDS, (w+1)*32*ROUNDS) of the tile (loads stay
-// coalesced: 32 consecutive keys per round), so ranking needs no CTA barrier per round:
-//   1. per round, warp match_any ranks equal digits among the lanes; a warp-private digit
-//      counter (shared memory, uint16) orders the rounds -> rank of each key within its
-//      warp's keys of that digit (kept in registers);
-//   2. one barrier; per digit, an exclusive scan of the 8 warp counters (warp order =
-//      index order) and of the tile's digit counts (tile-local run starts);
-//   3. each key's tile-local position = run start + warp prefix + in-warp rank: STAGED
-//      writes the tile digit-sorted into shared memory and then out coalesced (small digit
-//      sets), otherwise keys scatter straight to their global positions.
+// per pass (one CTA each): the global digit totals -> their exclusive scan (the digit's
+// first output position)
+__global__ void __launch_bounds__(kRsThreads) os_scan_kernel(const uint32_t* __restrict__ ghist,
+                                                            uint32_t* __restrict__ gofs, int dbits, int passes,
+                                                            int nlast) {
+    __shared__ uint32_t a[kRsMaxDigits];
+    __shared__ uint32_t s_ws[kRsThreads / 32];
+    const int ps = blockIdx.x;
+    const int nb = ps == passes - 1 ? nlast : 1 << dbits;
+    for (int d = threadIdx.x; d < nb; d += kRsThreads) a[d] = ghist[ps * kRsMaxDigits + d];
+    __syncthreads();
+    block_scan_smem(a, nb, s_ws);
+    for (int d = threadIdx.x; d < nb; d += kRsThreads) gofs[ps * kRsMaxDigits + d] = a[d];
+}
+
+// ---------------------------------------------------------------------------------
+// a2: stable LSD counting sort, ONE persistent cooperative kernel per pass.  Keys lie in
+// [0, nb] (nb = dropped); passes = ceil(bits/10) with digits of ceil(bits/passes) <= 10
+// bits, the LAST pass taking all the remaining high bits (its digit set (nb >> shift) + 1
+// holds the sentinel).
+//
+// The C CTAs of a pass are all resident (cooperative launch); CTA c owns the contiguous
+// tiles [c T / C, (c+1) T / C) of the keys, so the stable order is CTA order, then tile
+// order, then position within the tile:
+//   A. range histogram: the digit counts of the CTA's whole range -> rowhist[c][d] (for the
+//      first pass the convert kernel, which walks the same ranges, has written them);
+//   B. grid barrier; CTA c scans the columns d = c, c + C, ... over the C ranges (one warp per
+//      column) -> colpre[c'][d] = count of digit d in the ranges before c'; grid barrier;
+//   C. running offsets boff[d] = digit offset (the convert's global totals, scanned) +
+//      colpre[c][d]; then per tile, with no inter-CTA traffic:
+//      1. per round, warp match_any ranks equal digits among the lanes; a warp-private digit
+//         counter (shared memory, uint16) orders the rounds -> rank of each key within its
+//         warp's keys of that digit (warp w owns the contiguous sub-range
+//         [w*32*ROUNDS, (w+1)*32*ROUNDS) of the tile; loads stay coalesced);
+//      2. per digit, an exclusive scan of the 8 warp counters (warp order = index order)
+//         -> the tile's digit counts -> their exclusive scan = tile-local run starts;
+//      3. the tile is written digit-sorted into shared memory, then out coalesced, each run
+//         to boff[d]; boff[d] += the tile's count.
 // The result is the stable order (index order within equal digits), as the oracle's
 // std::stable_sort-equivalent definition requires.
-template <bool STAGED, int ROUNDS>
-__global__ void __launch_bounds__(kRsThreads) rs_downsweep(
-    const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
-    uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, int n, int shift, uint32_t dmask, int nbins,
-    const uint32_t* __restrict__ hscan, const uint32_t* __restrict__ dtot, int hstride) {
-    extern __shared__ uint32_t sm[];
+struct OsArgs {
+    const uint32_t* kin;
+    const uint32_t* vin;   // nullptr: values = input positions
+    uint32_t* kout;
+    uint32_t* vout;
+    int n, shift, nbins, ntiles, nctas;
+    uint32_t dmask;
+    const uint32_t* gofs;  // [nbins] exclusive scan of the digit totals
+    uint32_t* rowhist;     // [nctas][nbins] range histograms
+    uint32_t* colpre;      // [nctas][nbins] their column-wise exclusive scans
+    uint32_t* bar;         // grid-barrier arrival counter (zero at launch)
+};
+
+__device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
+    return *reinterpret_cast<const volatile uint32_t*>(p);
+}
+
+// mbarrier + 1-D TMA (cp.async.bulk) for the radix passes' tile prefetch
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void os_mbar_init(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n\tfence.mbarrier_init.release.cluster;" ::"r"(smem_addr(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void os_mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok = 0, polls = 0;
+    for (;;) {
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(smem_addr(bar)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (++polls > (1u << 26)) __trap();  // a copy that never lands is a bug: fail, don't hang
+    }
+}
+// bytes (multiple of 16, 16-byte aligned ends) global -> shared, completing on bar
+__device__ __forceinline__ void os_tma_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void os_mbar_expect(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+
+// all CTAs of a cooperative launch: every thread's prior global writes are visible to
+// every CTA after the call (the k-th barrier of the launch waits for k * gridDim.x arrivals)
+__device__ __forceinline__ void grid_barrier(uint32_t* bar, uint32_t target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(bar, 1u);
+        uint32_t polls = 0;
+        while (ld_volatile(bar) < target) {  // (all CTAs are resident: a hang is a bug -> trap)
+            __nanosleep(64);
+            if (++polls > (1u << 26)) __trap();
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <int ROUNDS, bool UPSWEEP>
+__global__ void __launch_bounds__(kRsThreads, ROUNDS >= 16 ? 2 : 3) os_pass_kernel(OsArgs a) {
+    extern __shared__ __align__(16) uint32_t sm[];
     __shared__ uint32_t s_ws[kRsThreads / 32];
+    __shared__ __align__(8) uint64_t s_bar;  // the prefetched tile has landed
     constexpr int kW = kRsThreads / 32;
     constexpr int tile = kRsThreads * ROUNDS;
-    uint32_t* boff = sm;                    // [nbins] global base of the tile's digit run
-    uint32_t* dstart = sm + nbins;          // [nbins] tile-local start of the digit run
-    uint32_t* skey = sm + 2 * nbins;        // [tile] (STAGED)
-    uint32_t* sval = skey + tile;           // [tile] (STAGED)
-    uint16_t* wcnt = reinterpret_cast<uint16_t*>(STAGED ? sval + tile : sm + 2 * nbins);  // [kW][nbins]
+    const int nbins = a.nbins, shift = a.shift, n = a.n;
+    const uint32_t dmask = a.dmask;
+    uint32_t* pre_k = sm;                   // [tile] the next tile's keys (TMA)
+    uint32_t* pre_v = sm + tile;            // [tile] and values
+    uint32_t* boff = sm + 2 * tile;         // [nbins] running global base of each digit
+    uint32_t* dstart = boff + nbins;        // [nbins] tile count -> tile-local start of the run
+    uint32_t* skey = dstart + nbins;        // [tile] the tile, digit-sorted
+    uint32_t* sval = skey + tile;           // [tile]
+    uint16_t* wcnt = reinterpret_cast<uint16_t*>(sval + tile);  // [kW][nbins]
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-    const int b = blockIdx.x;
-    for (int e = t; e < kW * nbins; e += kRsThreads) wcnt[e] = 0;
-    // this warp's keys (index order: round-major within the warp's sub-range)
-    const int wbase = b * tile + warp * 32 * ROUNDS + lane;
-    uint32_t kb[ROUNDS], vb[ROUNDS], rk[ROUNDS];
+    const int c = blockIdx.x, C = a.nctas;
+    const int tb = os_tile_begin(c, a.ntiles, C), te = os_tile_begin(c + 1, a.ntiles, C);
+    // A. the range histogram
+    if (UPSWEEP) {
+        for (int d = t; d < nbins; d += kRsThreads) boff[d] = 0u;
+        __syncthreads();
+        const int i0 = tb * tile, i1 = min(n, te * tile);  // i0 % 4 == 0
+        constexpr int kU = 4;                              // 16-byte loads in flight per thread
+        for (int i = i0 + 4 * t; i < i1; i += 4 * kU * kRsThreads) {
+            uint4 k4[kU];
 #pragma unroll
-    for (int r = 0; r < ROUNDS; r++) {
-        const int i = wbase + r * 32;
-        kb[r] = i < n ? kin[i] : 0u;
-        vb[r] = i < n ? (vin ? vin[i] : (uint32_t)i) : 0u;
+            for (int u = 0; u < kU; u++) {
+                const int j = i + u * 4 * kRsThreads;
+                k4[u] = j + 3 < i1 ? __ldcg(reinterpret_cast<const uint4*>(a.kin + j)) : make_uint4(0u, 0u, 0u, 0u);
+            }
+#pragma unroll
+            for (int u = 0; u < kU; u++) {
+                const int j = i + u * 4 * kRsThreads;
+                if (j + 3 < i1) {
+                    atomicAdd(&boff[(k4[u].x >> shift) & dmask], 1u);
+                    atomicAdd(&boff[(k4[u].y >> shift) & dmask], 1u);
+                    atomicAdd(&boff[(k4[u].z >> shift) & dmask], 1u);
+                    atomicAdd(&boff[(k4[u].w >> shift) & dmask], 1u);
+                } else {
+                    for (int e = j; e < i1; e++) atomicAdd(&boff[(a.kin[e] >> shift) & dmask], 1u);
+                }
+            }
+        }
+        __syncthreads();
+        for (int d = t; d < nbins; d += kRsThreads) a.rowhist[(size_t)c * nbins + d] = boff[d];
     }
-    __syncthreads();
+    // B. column scans over the ranges, between two grid barriers
+    grid_barrier(a.bar, (uint32_t)C);
+    for (int d = c + warp * C; d < nbins; d += kW * C) {
+        const int per = (C + 31) / 32;  // consecutive ranges per lane
+        uint32_t tot = 0;
+        for (int k = 0; k < per; k++) {
+            const int r = lane * per + k;
+            if (r < C) tot += __ldcg(a.rowhist + (size_t)r * nbins + d);
+        }
+        uint32_t inc = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
+        }
+        uint32_t pre = inc - tot;
+        for (int k = 0; k < per; k++) {
+            const int r = lane * per + k;
+            if (r < C) {
+                const uint32_t v = __ldcg(a.rowhist + (size_t)r * nbins + d);
+                a.colpre[(size_t)r * nbins + d] = pre;
+                pre += v;
+            }
+        }
+    }
+    grid_barrier(a.bar, 2u * (uint32_t)C);
+    // C. the range's tiles in order
+    for (int d = t; d < nbins; d += kRsThreads) boff[d] = a.gofs[d] + __ldcg(a.colpre + (size_t)c * nbins + d);
     uint16_t* my = wcnt + warp * nbins;
     const uint32_t lt = (1u << lane) - 1u;
-#pragma unroll
-    for (int r = 0; r < ROUNDS; r++) {
-        const bool valid = wbase + r * 32 < n;
-        const uint32_t d = valid ? ((kb[r] >> shift) & dmask) : (0x10000u + lane);  // unique if invalid
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
-        const uint32_t pre = valid ? (uint32_t)my[d] : 0u;
-        rk[r] = pre + __popc(peers & lt);
-        __syncwarp();
-        if (valid && (peers & lt) == 0) my[d] = (uint16_t)(pre + __popc(peers));
-        __syncwarp();
+    // tile b's keys (and values) stream into pre_k / pre_v by TMA while tile b - 1 is ranked
+    auto prefetch = [&](int b) {  // (thread 0)
+        const uint32_t bytes = (uint32_t)((min(tile, n - b * tile) * 4 + 15) & ~15);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after the generic reads
+        os_mbar_expect(&s_bar, a.vin ? 2 * bytes : bytes);
+        os_tma_load(pre_k, a.kin + (size_t)b * tile, bytes, &s_bar);
+        if (a.vin) os_tma_load(pre_v, a.vin + (size_t)b * tile, bytes, &s_bar);
+    };
+    if (t == 0) {
+        os_mbar_init(&s_bar);
+        if (tb < te) prefetch(tb);
     }
-    __syncthreads();
-    // per digit: warp counters -> exclusive prefixes over warps; tile count -> dstart
-    for (int d = t; d < nbins; d += kRsThreads) {
-        uint32_t run = 0;
+    __syncthreads();  // the barrier is initialised before anyone waits on it
+    for (int b = tb; b < te; b++) {
+        for (int e = t; e < kW * nbins; e += kRsThreads) wcnt[e] = 0;
+        const int wbase = b * tile + warp * 32 * ROUNDS + lane;
+        const int lbase = warp * 32 * ROUNDS + lane;
+        uint32_t kb[ROUNDS], vb[ROUNDS], rk[ROUNDS];
+        os_mbar_wait(&s_bar, (uint32_t)(b - tb) & 1u);
 #pragma unroll
-        for (int w = 0; w < kW; w++) {
-            const uint32_t c = wcnt[w * nbins + d];
-            wcnt[w * nbins + d] = (uint16_t)run;
-            run += c;
+        for (int r = 0; r < ROUNDS; r++) {
+            const int i = wbase + r * 32;
+            kb[r] = pre_k[lbase + r * 32];
+            vb[r] = a.vin ? pre_v[lbase + r * 32] : (uint32_t)i;
         }
-        dstart[d] = run;
-        boff[d] = dtot[d];  // -> exclusive scan of the digit totals
-    }
-    __syncthreads();
-    block_scan_smem(boff, nbins, s_ws);
-    if (STAGED) block_scan_smem(dstart, nbins, s_ws);
-    for (int d = t; d < nbins; d += kRsThreads) boff[d] += hscan[(size_t)d * hstride + b];  // + tile prefix
-    __syncthreads();
+        __syncthreads();  // wcnt zeroed; the previous tile's staging read out; pre_* read
+        if (t == 0 && b + 1 < te) prefetch(b + 1);
 #pragma unroll
-    for (int r = 0; r < ROUNDS; r++) {
-        if (wbase + r * 32 >= n) break;
-        const uint32_t d = (kb[r] >> shift) & dmask;
-        const uint32_t pos = (uint32_t)my[d] + rk[r];
-        if (STAGED) {
-            const uint32_t lp = dstart[d] + pos;
+        for (int r = 0; r < ROUNDS; r++) {
+            const bool valid = wbase + r * 32 < n;
+            const uint32_t d = valid ? ((kb[r] >> shift) & dmask) : (0x10000u + lane);  // unique if invalid
+            const uint32_t peers = __match_any_sync(0xffffffffu, d);
+            const uint32_t pre = valid ? (uint32_t)my[d] : 0u;
+            rk[r] = pre + __popc(peers & lt);
+            __syncwarp();
+            if (valid && (peers & lt) == 0) my[d] = (uint16_t)(pre + __popc(peers));
+            __syncwarp();
+        }
+        __syncthreads();
+        for (int d = t; d < nbins; d += kRsThreads) {
+            uint32_t run = 0;
+#pragma unroll
+            for (int w = 0; w < kW; w++) {
+                const uint32_t cnt = wcnt[w * nbins + d];
+                wcnt[w * nbins + d] = (uint16_t)run;
+                run += cnt;
+            }
+            dstart[d] = run;
+        }
+        __syncthreads();
+        block_scan_smem(dstart, nbins, s_ws);
+#pragma unroll
+        for (int r = 0; r < ROUNDS; r++) {
+            const int i = wbase + r * 32;
+            if (i >= n) break;
+            const uint32_t d = (kb[r] >> shift) & dmask;
+            const uint32_t lp = dstart[d] + (uint32_t)my[d] + rk[r];
             skey[lp] = kb[r];
             sval[lp] = vb[r];
-        } else {
-            const uint32_t dst = boff[d] + pos;
-            kout[dst] = kb[r];
-            vout[dst] = vb[r];
         }
-    }
-    if (!STAGED) return;
-    __syncthreads();
-    const int base = b * tile;
-    const int cnt = min(tile, n - base);
-    for (int e = t; e < cnt; e += kRsThreads) {
-        const uint32_t k = skey[e];
-        const uint32_t d = (k >> shift) & dmask;
-        const uint32_t dst = boff[d] + (uint32_t)e - dstart[d];
-        kout[dst] = k;
-        vout[dst] = sval[e];
+        __syncthreads();
+        const int cnt = min(tile, n - b * tile);
+        for (int e = t; e < cnt; e += kRsThreads) {
+            const uint32_t k = skey[e];
+            const uint32_t d = (k >> shift) & dmask;
+            const uint32_t dst = boff[d] + (uint32_t)e - dstart[d];
+            a.kout[dst] = k;
+            a.vout[dst] = sval[e];
+        }
+        __syncthreads();
+        for (int d = t; d < nbins; d += kRsThreads)  // + the tile's count of d
+            boff[d] += (d + 1 < nbins ? dstart[d + 1] : (uint32_t)cnt) - dstart[d];
     }
 }
 
-// Per-digit exclusive scan over the tiles, in place (hist is digit-major [d][stride], rows
-// 16-byte aligned), one CTA per digit: coalesced uint4 loads of 1024 tiles per step, a block
-// scan, a running carry; dtot[d] = the digit's total.
+// Exclusive scan of one row of counts in place + its total (band compaction's block
+// offsets), one CTA: coalesced uint4 loads of 1024 entries per step, a block scan, a carry.
 __global__ void __launch_bounds__(256) rs_scan_digits(uint32_t* __restrict__ hist, int nbins, int ntiles,
                                                       int stride, uint32_t* __restrict__ dtot) {
     __shared__ uint32_t s_ws[8];
@@ -340,6 +517,7 @@ __global__ void __launch_bounds__(256) rs_scan_digits(uint32_t* __restrict__ his
         carry += tot;
     }
     if (t == 0) dtot[d] = carry;
+    (void)nbins;
 }
 
 // a2 gather + bucket offsets, one pass over the sorted keys.  Position d in [0, n]:
@@ -566,7 +744,7 @@ static int bin_sorted(kde_ctx* c, const double* d_x, const double* d_y, int n) {
     cudaStream_t s = c->stream;
     const uint32_t nb = (uint32_t)g.nbx * (uint32_t)g.nby;
     // LSD passes over the keys [0, nb] (nb = dropped).  The real keys [0, nb) need kb bits;
-    // passes = ceil(kb / 11), digits of db = ceil(kb / passes) bits, and the LAST pass takes
+    // passes = ceil(kb / 10), digits of db = ceil(kb / passes) bits, and the LAST pass takes
     // all the remaining high bits, key >> shift in [0, nb >> shift] -- a digit set of
     // (nb >> shift) + 1 that holds the dropped sentinel without an extra pass (C4: 2^20
     // buckets -> 1024 + 1025 digits, two passes instead of three).
@@ -574,86 +752,106 @@ static int bin_sorted(kde_ctx* c, const double* d_x, const double* d_y, int n) {
     while ((1ull << kb) < nb) kb++;
     const int passes = (kb + kRsMaxBits - 1) / kRsMaxBits;
     const int dbits = (kb + passes - 1) / passes;
+    if (passes > kRsMaxPasses || n64 >= (1ll << 30)) {
+        set_error("binning: %d key bits / %lld points not supported", kb, (long long)n64);
+        return KDE_EUNSUPPORTED;
+    }
     auto pass_bins = [&](int ps) {
         return ps == passes - 1 ? (int)(nb >> (ps * dbits)) + 1 : 1 << dbits;
     };
     auto pass_mask = [&](int ps) { return ps == passes - 1 ? 0xffffffffu : (1u << dbits) - 1u; };
     int nbins = 0;  // the largest digit set
     for (int ps = 0; ps < passes; ps++) nbins = std::max(nbins, pass_bins(ps));
-    const uint32_t dmask0 = pass_mask(0);
-    const int nbins0 = pass_bins(0);
-    // tuning knobs (A/B experiments): KDE_RS_ROUNDS = 8|16 forces the tile rounds,
-    // KDE_RS_STAGED = the largest digit count that stages the tile in shared memory
+    // tuning knob (A/B experiments): KDE_RS_ROUNDS = 8|16 forces the tile rounds.  Default:
+    // 4096-key tiles from 8 M points on (C2 prefers 2048-key tiles: more CTAs for its 2 M
+    // keys); tiles hold >= 4 keys per digit
     static const int env_rounds = getenv("KDE_RS_ROUNDS") ? atoi(getenv("KDE_RS_ROUNDS")) : 0;
-    static const int env_staged = getenv("KDE_RS_STAGED") ? atoi(getenv("KDE_RS_STAGED")) : 1100;
-    // default: 4096-key tiles from 8 M points on (measured: C4 binning 0.96 -> 0.91 ms; C2
-    // prefers 2048-key tiles: more CTAs for its 2 M keys); tiles hold >= 4 keys per digit
     const int rounds = (env_rounds == 8 || env_rounds == 16) ? std::max(env_rounds, rs_rounds(nbins))
                        : (n >= (8 << 20) ? std::max(16, rs_rounds(nbins)) : rs_rounds(nbins));
-    if (rounds != 8 && rounds != 16 && rounds != 32) {
+    if (rounds != 8 && rounds != 16) {
         set_error("binning: %d digits per pass not supported", nbins);
         return KDE_EUNSUPPORTED;
     }
     const int tile = kRsThreads * rounds;
     const int nblk = (n + tile - 1) / tile;
-    const int hstride = (nblk + 3) & ~3;  // histogram rows: 16-byte aligned (rs_scan_digits)
     if (n64 > pb.cap || pb.key[0] == nullptr) {
         const int64_t cap = n64 > 1024 ? n64 : 1024;
         int rc = KDE_OK;
-        rc |= grow((void**)&pb.key[0], sizeof(uint32_t) * cap);
-        rc |= grow((void**)&pb.key[1], sizeof(uint32_t) * cap);
-        rc |= grow((void**)&pb.val[0], sizeof(uint32_t) * cap);
-        rc |= grow((void**)&pb.val[1], sizeof(uint32_t) * cap);
+        rc |= grow((void**)&pb.key[0], sizeof(uint32_t) * (cap + 4));  // + TMA tail
+        rc |= grow((void**)&pb.key[1], sizeof(uint32_t) * (cap + 4));  // + TMA tail
+        rc |= grow((void**)&pb.val[0], sizeof(uint32_t) * (cap + 4));  // + TMA tail
+        rc |= grow((void**)&pb.val[1], sizeof(uint32_t) * (cap + 4));  // + TMA tail
         rc |= grow((void**)&pb.xy, sizeof(float2) * cap);
         rc |= grow((void**)&pb.rng, sizeof(uint2) * cap);
         rc |= grow((void**)&pb.rec, sizeof(uint4) * cap);
         if (rc) return KDE_ENOMEM;
         pb.cap = cap;
     }
-    const int64_t hneed = (int64_t)nbins * (hstride > 0 ? hstride : 4);
-    if (hneed > pb.hist_cap) {
-        if (grow((void**)&pb.hist, sizeof(uint32_t) * hneed)) return KDE_ENOMEM;
-        if (grow((void**)&pb.scan_tmp, sizeof(uint32_t) * 4096)) return KDE_ENOMEM;  // digit totals
-        pb.hist_cap = hneed;
+    // hist: [passes][1025] totals, [passes][1025] their scans, a grid-barrier counter per pass
+    constexpr int kHistWords = 2 * kRsMaxPasses * kRsMaxDigits + kRsMaxPasses + 1;
+    if (!pb.hist && grow((void**)&pb.hist, sizeof(uint32_t) * kHistWords)) return KDE_ENOMEM;
+    uint32_t* ghist = pb.hist;
+    uint32_t* gofs = pb.hist + kRsMaxPasses * kRsMaxDigits;
+    uint32_t* bars = pb.hist + 2 * kRsMaxPasses * kRsMaxDigits;
+    // the passes' CTA count: every CTA resident (cooperative launch), at most one per tile
+    const size_t dsmem = sizeof(uint32_t) * (2 * nbins + 4 * tile) + sizeof(uint16_t) * 8 * nbins;
+    auto k_first = rounds == 8 ? os_pass_kernel<8, false> : os_pass_kernel<16, false>;
+    auto k_next = rounds == 8 ? os_pass_kernel<8, true> : os_pass_kernel<16, true>;
+    int nsm = 148, occ0 = 0, occ1 = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->p.device);
+    // the shared-memory opt-in is per device and cheap: set it on every load (no
+    // process-global state)
+    cudaFuncSetAttribute(k_first, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem);
+    cudaFuncSetAttribute(k_next, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ0, k_first, kRsThreads, dsmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_next, kRsThreads, dsmem);
+    const int nctas = std::max(1, std::min(nblk, nsm * std::min(occ0, occ1)));
+    if (std::min(occ0, occ1) < 1) {
+        set_error("binning: radix pass kernel does not fit an SM");
+        return KDE_EUNSUPPORTED;
+    }
+    const int64_t sneed = (int64_t)nctas * nbins;  // range histograms / column scans
+    if (sneed > pb.ost_cap) {
+        const int64_t cap = std::max<int64_t>(sneed, (int64_t)nsm * 3 * kRsMaxDigits);
+        for (int k = 0; k < 2; k++)
+            if (grow((void**)&pb.ost[k], sizeof(uint32_t) * cap)) return KDE_ENOMEM;
+        pb.ost_cap = cap;
     }
     cudaMemsetAsync(c->d_stats, 0, 3 * sizeof(unsigned long long), s);
     if (n > 0) {
-        // small digit sets scatter short runs: stage the tile digit-sorted in shared memory
-        // and write it out coalesced; large ones scatter directly
-        auto dn_smem = [&](int nbp, bool stg) {
-            return sizeof(uint32_t) * (2 * nbp + (stg ? 2 * tile : 0)) + sizeof(uint16_t) * 8 * nbp;
-        };
-        {   // the shared-memory opt-in is per device and cheap: set it on every load (no
-            // process-global state).  Largest case: 2049 digits, tile 8192.
-            const int mx = (int)std::max(dn_smem(2049, false), dn_smem(1100, true));
-            cudaFuncSetAttribute(rs_downsweep<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-            cudaFuncSetAttribute(rs_downsweep<true, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-            cudaFuncSetAttribute(rs_downsweep<false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-            cudaFuncSetAttribute(rs_downsweep<false, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-            cudaFuncSetAttribute(rs_downsweep<false, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        }
-        bin_convert_kernel<<<nblk, kRsThreads, sizeof(uint32_t) * nbins0, s>>>(
-            d_x, d_y, n, g, nb, pb.key[0], pb.rec, c->d_stats, dmask0, nbins0, pb.hist, hstride, rounds);
-        c->launches += 1;
+        cudaMemsetAsync(ghist, 0, sizeof(uint32_t) * kRsMaxPasses * kRsMaxDigits, s);
+        cudaMemsetAsync(bars, 0, sizeof(uint32_t) * kRsMaxPasses, s);
+        // the convert: each pass-0 range cut into `split` parts (~4 CTAs per SM), the parts'
+        // digit counts added into the range histogram
+        const int split = std::max(1, std::min(4, (nsm * 4) / nctas));
+        cudaMemsetAsync(pb.ost[0], 0, sizeof(uint32_t) * (size_t)nctas * pass_bins(0), s);
+        bin_convert_kernel<<<nctas * split, kRsThreads, 0, s>>>(d_x, d_y, n, g, nb, pb.key[0], pb.rec, c->d_stats,
+                                                                passes, dbits, ghist, tile, nblk, pb.ost[0],
+                                                                pass_bins(0), split);
+        os_scan_kernel<<<passes, kRsThreads, 0, s>>>(ghist, gofs, dbits, passes, pass_bins(passes - 1));
+        c->launches += 2;
         int cur = 0;
         for (int ps = 0; ps < passes; ps++) {
-            const int shift = ps * dbits;
-            const uint32_t dmask = pass_mask(ps);
-            const int nbp = pass_bins(ps);
-            if (ps > 0) {
-                rs_upsweep<<<nblk, kRsThreads, sizeof(uint32_t) * nbp, s>>>(pb.key[cur], n, shift, dmask, nbp,
-                                                                           pb.hist, hstride, rounds);
-                c->launches += 1;
-            }
-            rs_scan_digits<<<nbp, 256, 0, s>>>(pb.hist, nbp, nblk, hstride, pb.scan_tmp);
-            const bool staged = nbp <= env_staged && rounds <= 16;
-            auto dsw = staged ? (rounds == 8 ? rs_downsweep<true, 8> : rs_downsweep<true, 16>)
-                              : (rounds == 8 ? rs_downsweep<false, 8>
-                                             : rounds == 16 ? rs_downsweep<false, 16> : rs_downsweep<false, 32>);
-            dsw<<<nblk, kRsThreads, dn_smem(nbp, staged), s>>>(pb.key[cur], ps == 0 ? nullptr : pb.val[cur],
-                                                                 pb.key[cur ^ 1], pb.val[cur ^ 1], n, shift, dmask,
-                                                                 nbp, pb.hist, pb.scan_tmp, hstride);
-            c->launches += 2;
+            OsArgs oa;
+            oa.kin = pb.key[cur];
+            oa.vin = ps == 0 ? nullptr : pb.val[cur];
+            oa.kout = pb.key[cur ^ 1];
+            oa.vout = pb.val[cur ^ 1];
+            oa.n = n;
+            oa.shift = ps * dbits;
+            oa.nbins = pass_bins(ps);
+            oa.ntiles = nblk;
+            oa.nctas = nctas;
+            oa.dmask = pass_mask(ps);
+            oa.gofs = gofs + ps * kRsMaxDigits;
+            oa.rowhist = pb.ost[0];
+            oa.colpre = pb.ost[1];
+            oa.bar = bars + ps;
+            void* args[] = {&oa};
+            const cudaError_t le = cudaLaunchCooperativeKernel((const void*)(ps == 0 ? k_first : k_next), dim3(nctas),
+                                                               dim3(kRsThreads), args, dsmem, s);
+            if (le != cudaSuccess) return cuda_fail(le, "radix pass (cooperative launch)");
+            c->launches += 1;
             cur ^= 1;
         }
         pb.perm = pb.val[cur];

@@ -560,6 +560,7 @@ int launch_direct(kde_ctx* c, float* out, cudaStream_t s) {
     tmark(c, 3, s);
     fn(a, pl.mt, pl.grid, s);  // persistent; the item count is on the device
     c->launches += 1;
+    c->main_kernel = 1;
     tmark(c, 4, s);
     launch_combine(c, pl, out, s);
     tmark(c, 5, s);

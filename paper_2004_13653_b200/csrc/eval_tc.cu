@@ -447,8 +447,10 @@ int launch_tc(kde_ctx* c, float* out, cudaStream_t s, bool split) {
         {launch_tc_h<1, 0, true, true>, launch_tc_h<1, 1, true, true>, launch_tc_h<1, 2, true, true>,
          launch_tc_h<1, 3, true, true>, launch_tc_h<1, 4, true, true>, launch_tc_h<1, 5, true, true>,
          launch_tc_h<1, 6, true, true>, launch_tc_h<1, 7, true, true>}};
+    cudaMemsetAsync(pl.d_totals + kTotChunksExec, 0, sizeof(int), s);  // set by eval_tc5.cu only
     const int rc5 = split ? KDE_EUNSUPPORTED : launch_tc5(c, s);  // eval_tc5.cu when it applies
     if (rc5 != KDE_OK && rc5 != KDE_EUNSUPPORTED) return rc5;
+    c->main_kernel = rc5 == KDE_OK ? 3 : 2;
     if (rc5 == KDE_OK)
         ;
     else if (c->kern == KDE_GAUSSIAN && !rec)

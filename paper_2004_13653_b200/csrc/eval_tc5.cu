@@ -419,6 +419,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc5_kernel(const Args a) {
             nitem++;
         }
         if (lane == 0) {
+            if (q) atomicAdd(&a.totals[kTotChunksExec], q);  // executed chunks (kde_stats.tc_mma_flops)
             __threadfence_block();
             s_post[w] = -1 - nitem;  // done after nitem items
         }

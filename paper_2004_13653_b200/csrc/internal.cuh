@@ -52,9 +52,12 @@ struct PointBufs {
     int stage = 0;                             // staging buffer of the next host load
     uint32_t *key[2] = {nullptr, nullptr};     // radix ping-pong
     uint32_t *val[2] = {nullptr, nullptr};
-    uint32_t *hist = nullptr;                  // radix per-(digit, block) counts
-    int64_t hist_cap = 0;
-    uint32_t *scan_tmp = nullptr;                // radix digit totals
+    uint32_t *hist = nullptr;                  // radix: per-pass digit totals, their exclusive
+                                               // scans, grid-barrier counters (bin.cu)
+    uint32_t *ost[2] = {nullptr, nullptr};     // radix: per-CTA range histograms, their
+                                               // column-wise exclusive scans [cta][digit]
+    int64_t ost_cap = 0;                       // words per buffer
+    uint32_t *scan_tmp = nullptr;                // band compaction: kept total
     uint4 *rec = nullptr;                      // per input point: lx, ly, packed ranges
     float2 *xy = nullptr;                      // sorted bucket-local coordinates
     uint2 *rng = nullptr;                      // sorted packed int16 ranges
@@ -138,7 +141,9 @@ constexpr int kTotHot = 4;     // split groups (segment reduce list length)
 constexpr int kTotChunks = 5;  // tensor-core path: chunk_pts-point MMA chunks (executed flops)
 constexpr int kTotQueue = 6;   // persistent-kernel work-queue head (CTA items)
 constexpr int kTotQueue2 = 7;  // second queue head (direct path: per-warp items)
-constexpr int kTotInts = 8;
+constexpr int kTotChunksExec = 8;  // chunks the per-warp tensor-core kernel executed (eval_tc5.cu's
+                                   // bucket-homogeneous chunks; 0 when the other kernel ran)
+constexpr int kTotInts = 9;
 
 // Upper bound on a path's items/slots for n points: every full segment, plus per
 // non-empty group its remainder pieces (at most n / part_pts + one per group), times the
@@ -180,6 +185,7 @@ struct kde_ctx {
                                                // n_in, or n_finite after a banded load (so a
                                                // NaN-padded point shard plans like the raw set)
     int64_t launches = 0;                      // kernels launched (kde_stats.kernel_launches)
+    int main_kernel = 0;                       // kde_stats.main_kernel of the last eval
     bool timing = false;                       // record phase events (kde_set_timing)
     cudaEvent_t tev[6] = {};                   // bin0, bin1 (load); plan0, main0, main1, comb1 (eval)
     bool tev_load = false, tev_eval = false;
