@@ -569,7 +569,8 @@ int kde_get_bins(const kde_ctx* c, int64_t* offsets, int64_t* perm, float* lx, f
     cudaError_t e = cudaSuccess;
     if (perm) {
         pv.resize(m);
-        e = cudaMemcpy(pv.data(), c->pb.perm, sizeof(uint32_t) * m, cudaMemcpyDeviceToHost);
+        e = cudaMemcpy2D(pv.data(), sizeof(uint32_t), reinterpret_cast<const char*>(c->pb.sorted) + sizeof(uint32_t),
+                         sizeof(uint2), sizeof(uint32_t), m, cudaMemcpyDeviceToHost);  // the pairs' second words
         if (e == cudaSuccess && c->pb.compacted) {  // banded: sorted compacted positions -> input indices
             std::vector<uint32_t> ci((size_t)c->stats.n_in);
             e = cudaMemcpy(ci.data(), c->pb.cidx, sizeof(uint32_t) * ci.size(), cudaMemcpyDeviceToHost);
@@ -805,15 +806,13 @@ void kde_free(kde_ctx* c) {
         cudaFree(pb.sx[k]);
         cudaFree(pb.sy[k]);
     }
-    for (int k = 0; k < 2; k++) {
-        cudaFree(pb.key[k]);
-        cudaFree(pb.val[k]);
-    }
+    cudaFree(pb.key[0]);
+    for (int k = 0; k < 2; k++) cudaFree(pb.pair[k]);
+    cudaFree(pb.rec);
     cudaFree(pb.hist);
     cudaFree(pb.ost[0]);
     cudaFree(pb.ost[1]);
     cudaFree(pb.scan_tmp);
-    cudaFree(pb.rec);
     cudaFree(pb.xy);
     cudaFree(pb.rng);
     cudaFree(pb.cx);

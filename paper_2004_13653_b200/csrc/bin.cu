@@ -104,18 +104,17 @@ __host__ __device__ inline int os_tile_begin(int c, int ntiles, int nctas) {
     return (int)(((int64_t)c * ntiles) / nctas);
 }
 
-// a1 kernel: each CTA converts the contiguous range of whole sort tiles the first radix
-// pass's CTA of the same index sorts.  Keys, the point's
-// record (bucket-local fp32 coordinates + packed int16 ranges, read back by the gather), the
-// integer stats (n_finite, n_outside, useful_pairs), and the GLOBAL histogram of every radix
+// a1 kernel: each CTA converts (a part of) the contiguous range of whole sort tiles the
+// first radix pass's CTA of the same index sorts.  Keys, the point's record (bucket-local
+// fp32 coordinates + packed int16 ranges, read back by the gather), the integer stats (n_finite, n_outside, useful_pairs), and the GLOBAL histogram of every radix
 // pass's digit (shared-memory counts, one global add per nonzero count per CTA): the
 // radix passes take the digit offsets from these totals; the first pass's range histogram
 // is this CTA's count of its digit.
 __global__ void __launch_bounds__(kRsThreads, 4) bin_convert_kernel(
     const double* __restrict__ x, const double* __restrict__ y, int n, Geom g, uint32_t sentinel,
-    uint32_t* __restrict__ key, uint4* __restrict__ rec, unsigned long long* __restrict__ stats,
-    int passes, int dbits, uint32_t* __restrict__ ghist, int tile, int ntiles, uint32_t* __restrict__ rowhist0,
-    int nbins0, int split) {
+    uint32_t* __restrict__ key, uint4* __restrict__ rec, unsigned long long* __restrict__ stats, int passes,
+    int dbits, uint32_t* __restrict__ ghist, int tile, int ntiles, uint32_t* __restrict__ rowhist0, int nbins0,
+    int split) {
     __shared__ uint32_t h[kRsMaxPasses * kRsMaxDigits];
     for (int d = threadIdx.x; d < passes * kRsMaxDigits; d += kRsThreads) h[d] = 0;
     unsigned long long nf = 0, no = 0, up = 0;
@@ -251,10 +250,9 @@ __global__ void __launch_bounds__(kRsThreads) os_scan_kernel(const uint32_t* __r
 // The result is the stable order (index order within equal digits), as the oracle's
 // std::stable_sort-equivalent definition requires.
 struct OsArgs {
-    const uint32_t* kin;
-    const uint32_t* vin;   // nullptr: values = input positions
-    uint32_t* kout;
-    uint32_t* vout;
+    const uint32_t* kin;   // first pass: the keys (values = input positions)
+    const uint2* pin;      // later passes: (key, value) pairs
+    uint2* pout;           // (key, value) pairs, sorted by this pass's digit
     int n, shift, nbins, ntiles, nctas;
     uint32_t dmask;
     const uint32_t* gofs;  // [nbins] exclusive scan of the digit totals
@@ -323,39 +321,35 @@ __global__ void __launch_bounds__(kRsThreads, ROUNDS >= 16 ? 2 : 3) os_pass_kern
     constexpr int tile = kRsThreads * ROUNDS;
     const int nbins = a.nbins, shift = a.shift, n = a.n;
     const uint32_t dmask = a.dmask;
-    uint32_t* pre_k = sm;                   // [tile] the next tile's keys (TMA)
-    uint32_t* pre_v = sm + tile;            // [tile] and values
-    uint32_t* boff = sm + 2 * tile;         // [nbins] running global base of each digit
-    uint32_t* dstart = boff + nbins;        // [nbins] tile count -> tile-local start of the run
-    uint32_t* skey = dstart + nbins;        // [tile] the tile, digit-sorted
-    uint32_t* sval = skey + tile;           // [tile]
-    uint16_t* wcnt = reinterpret_cast<uint16_t*>(sval + tile);  // [kW][nbins]
+    uint2* pre = reinterpret_cast<uint2*>(sm);            // [tile] the next tile (TMA): pairs, or keys
+    uint2* spair = pre + tile;                            // [tile] the tile, digit-sorted
+    uint32_t* boff = reinterpret_cast<uint32_t*>(spair + tile);  // [nbins] running global base
+    uint32_t* dstart = boff + nbins;                      // [nbins] tile count -> tile-local run start
+    uint16_t* wcnt = reinterpret_cast<uint16_t*>(dstart + nbins);  // [kW][nbins]
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const int c = blockIdx.x, C = a.nctas;
     const int tb = os_tile_begin(c, a.ntiles, C), te = os_tile_begin(c + 1, a.ntiles, C);
-    // A. the range histogram
+    // A. the range histogram (the keys are the pairs' first words)
     if (UPSWEEP) {
         for (int d = t; d < nbins; d += kRsThreads) boff[d] = 0u;
         __syncthreads();
-        const int i0 = tb * tile, i1 = min(n, te * tile);  // i0 % 4 == 0
-        constexpr int kU = 4;                              // 16-byte loads in flight per thread
-        for (int i = i0 + 4 * t; i < i1; i += 4 * kU * kRsThreads) {
-            uint4 k4[kU];
+        const int i0 = tb * tile, i1 = min(n, te * tile);  // i0 even
+        constexpr int kU = 4;                              // 16-byte loads (2 pairs) in flight per thread
+        for (int i = i0 + 2 * t; i < i1; i += 2 * kU * kRsThreads) {
+            uint4 p4[kU];
 #pragma unroll
             for (int u = 0; u < kU; u++) {
-                const int j = i + u * 4 * kRsThreads;
-                k4[u] = j + 3 < i1 ? __ldcg(reinterpret_cast<const uint4*>(a.kin + j)) : make_uint4(0u, 0u, 0u, 0u);
+                const int j = i + u * 2 * kRsThreads;
+                p4[u] = j + 1 < i1 ? __ldcg(reinterpret_cast<const uint4*>(a.pin + j)) : make_uint4(0u, 0u, 0u, 0u);
             }
 #pragma unroll
             for (int u = 0; u < kU; u++) {
-                const int j = i + u * 4 * kRsThreads;
-                if (j + 3 < i1) {
-                    atomicAdd(&boff[(k4[u].x >> shift) & dmask], 1u);
-                    atomicAdd(&boff[(k4[u].y >> shift) & dmask], 1u);
-                    atomicAdd(&boff[(k4[u].z >> shift) & dmask], 1u);
-                    atomicAdd(&boff[(k4[u].w >> shift) & dmask], 1u);
-                } else {
-                    for (int e = j; e < i1; e++) atomicAdd(&boff[(a.kin[e] >> shift) & dmask], 1u);
+                const int j = i + u * 2 * kRsThreads;
+                if (j + 1 < i1) {
+                    atomicAdd(&boff[(p4[u].x >> shift) & dmask], 1u);
+                    atomicAdd(&boff[(p4[u].z >> shift) & dmask], 1u);
+                } else if (j < i1) {
+                    atomicAdd(&boff[(a.pin[j].x >> shift) & dmask], 1u);
                 }
             }
         }
@@ -377,13 +371,13 @@ __global__ void __launch_bounds__(kRsThreads, ROUNDS >= 16 ? 2 : 3) os_pass_kern
             const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
             if (lane >= o) inc += v;
         }
-        uint32_t pre = inc - tot;
+        uint32_t pre_ = inc - tot;
         for (int k = 0; k < per; k++) {
             const int r = lane * per + k;
             if (r < C) {
                 const uint32_t v = __ldcg(a.rowhist + (size_t)r * nbins + d);
-                a.colpre[(size_t)r * nbins + d] = pre;
-                pre += v;
+                a.colpre[(size_t)r * nbins + d] = pre_;
+                pre_ += v;
             }
         }
     }
@@ -392,13 +386,15 @@ __global__ void __launch_bounds__(kRsThreads, ROUNDS >= 16 ? 2 : 3) os_pass_kern
     for (int d = t; d < nbins; d += kRsThreads) boff[d] = a.gofs[d] + __ldcg(a.colpre + (size_t)c * nbins + d);
     uint16_t* my = wcnt + warp * nbins;
     const uint32_t lt = (1u << lane) - 1u;
-    // tile b's keys (and values) stream into pre_k / pre_v by TMA while tile b - 1 is ranked
+    const bool pairs_in = a.pin != nullptr;
+    // tile b (keys, or pairs) streams into `pre` by TMA while tile b - 1 is ranked
     auto prefetch = [&](int b) {  // (thread 0)
-        const uint32_t bytes = (uint32_t)((min(tile, n - b * tile) * 4 + 15) & ~15);
+        const int cnt = min(tile, n - b * tile);
+        const uint32_t bytes = (uint32_t)((cnt * (pairs_in ? 8 : 4) + 15) & ~15);  // (+ slack in the buffers)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after the generic reads
-        os_mbar_expect(&s_bar, a.vin ? 2 * bytes : bytes);
-        os_tma_load(pre_k, a.kin + (size_t)b * tile, bytes, &s_bar);
-        if (a.vin) os_tma_load(pre_v, a.vin + (size_t)b * tile, bytes, &s_bar);
+        os_mbar_expect(&s_bar, bytes);
+        if (pairs_in) os_tma_load(pre, a.pin + (size_t)b * tile, bytes, &s_bar);
+        else os_tma_load(pre, a.kin + (size_t)b * tile, bytes, &s_bar);
     };
     if (t == 0) {
         os_mbar_init(&s_bar);
@@ -411,23 +407,40 @@ __global__ void __launch_bounds__(kRsThreads, ROUNDS >= 16 ? 2 : 3) os_pass_kern
         const int lbase = warp * 32 * ROUNDS + lane;
         uint32_t kb[ROUNDS], vb[ROUNDS], rk[ROUNDS];
         os_mbar_wait(&s_bar, (uint32_t)(b - tb) & 1u);
+        if (pairs_in) {
 #pragma unroll
-        for (int r = 0; r < ROUNDS; r++) {
-            const int i = wbase + r * 32;
-            kb[r] = pre_k[lbase + r * 32];
-            vb[r] = a.vin ? pre_v[lbase + r * 32] : (uint32_t)i;
+            for (int r = 0; r < ROUNDS; r++) {
+                const uint2 pr = pre[lbase + r * 32];
+                kb[r] = pr.x;
+                vb[r] = pr.y;
+            }
+        } else {
+            const uint32_t* pk = reinterpret_cast<const uint32_t*>(pre);
+#pragma unroll
+            for (int r = 0; r < ROUNDS; r++) {
+                kb[r] = pk[lbase + r * 32];
+                vb[r] = (uint32_t)(wbase + r * 32);
+            }
         }
-        __syncthreads();  // wcnt zeroed; the previous tile's staging read out; pre_* read
-        if (t == 0 && b + 1 < te) prefetch(b + 1);
+        // the lanes holding each key's digit in its round: independent of the counters
 #pragma unroll
         for (int r = 0; r < ROUNDS; r++) {
             const bool valid = wbase + r * 32 < n;
             const uint32_t d = valid ? ((kb[r] >> shift) & dmask) : (0x10000u + lane);  // unique if invalid
-            const uint32_t peers = __match_any_sync(0xffffffffu, d);
-            const uint32_t pre = valid ? (uint32_t)my[d] : 0u;
-            rk[r] = pre + __popc(peers & lt);
+            rk[r] = __match_any_sync(0xffffffffu, d);
+        }
+        __syncthreads();  // wcnt zeroed; the previous tile's staging read out; `pre` read
+        if (t == 0 && b + 1 < te) prefetch(b + 1);
+        // the warp's counters, round by round: rank = counter + earlier peers in the round
+#pragma unroll
+        for (int r = 0; r < ROUNDS; r++) {
+            const bool valid = wbase + r * 32 < n;
+            const uint32_t d = (kb[r] >> shift) & dmask;
+            const uint32_t peers = rk[r];
+            const uint32_t pre_ = valid ? (uint32_t)my[d] : 0u;
+            rk[r] = pre_ + __popc(peers & lt);
             __syncwarp();
-            if (valid && (peers & lt) == 0) my[d] = (uint16_t)(pre + __popc(peers));
+            if (valid && (peers & lt) == 0) my[d] = (uint16_t)(pre_ + __popc(peers));
             __syncwarp();
         }
         __syncthreads();
@@ -445,21 +458,16 @@ __global__ void __launch_bounds__(kRsThreads, ROUNDS >= 16 ? 2 : 3) os_pass_kern
         block_scan_smem(dstart, nbins, s_ws);
 #pragma unroll
         for (int r = 0; r < ROUNDS; r++) {
-            const int i = wbase + r * 32;
-            if (i >= n) break;
+            if (wbase + r * 32 >= n) break;
             const uint32_t d = (kb[r] >> shift) & dmask;
-            const uint32_t lp = dstart[d] + (uint32_t)my[d] + rk[r];
-            skey[lp] = kb[r];
-            sval[lp] = vb[r];
+            spair[dstart[d] + (uint32_t)my[d] + rk[r]] = make_uint2(kb[r], vb[r]);
         }
         __syncthreads();
         const int cnt = min(tile, n - b * tile);
         for (int e = t; e < cnt; e += kRsThreads) {
-            const uint32_t k = skey[e];
-            const uint32_t d = (k >> shift) & dmask;
-            const uint32_t dst = boff[d] + (uint32_t)e - dstart[d];
-            a.kout[dst] = k;
-            a.vout[dst] = sval[e];
+            const uint2 pr = spair[e];
+            const uint32_t d = (pr.x >> shift) & dmask;
+            a.pout[boff[d] + (uint32_t)e - dstart[d]] = pr;
         }
         __syncthreads();
         for (int d = t; d < nbins; d += kRsThreads)  // + the tile's count of d
@@ -525,12 +533,12 @@ __global__ void __launch_bounds__(256) rs_scan_digits(uint32_t* __restrict__ his
 //            buckets (key[d-1], key[d]] (empty buckets take the next occupied bucket's start;
 //            long runs of empty buckets are written by the whole warp);
 //   gather:  a kept point (key < nb) at sorted position d gets its bucket-local fp32 SoA and
-//            packed int16 ranges from the record the convert kernel wrote in input order.
+//            packed int16 ranges from the record the convert kernel wrote in input order
+//            (measured: recomputing them from the fp64 coordinates instead is slower).
 // Kept keys (< nb) sort before the dropped sentinel nb, so positions [0, n_binned) are the
 // binned points.
 __global__ void __launch_bounds__(256) gather_offsets_kernel(const uint4* __restrict__ rec,
-                                                             const uint32_t* __restrict__ perm,
-                                                             const uint32_t* __restrict__ skey, int n, uint32_t nb,
+                                                             const uint2* __restrict__ sp, int n, uint32_t nb,
                                                              uint32_t* __restrict__ offsets,
                                                              float2* __restrict__ xy, uint2* __restrict__ rng) {
     const int lane = threadIdx.x & 31;
@@ -542,9 +550,10 @@ __global__ void __launch_bounds__(256) gather_offsets_kernel(const uint4* __rest
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const int d = d0 + u * blockDim.x + (threadIdx.x & ~31) + lane;
-            kc[u] = d < n ? skey[d] : nb;
-            kp[u] = (d > 0 && d <= n) ? skey[d - 1] : 0xffffffffu;
-            q[u] = (d < n && kc[u] < nb) ? perm[d] : 0u;
+            const uint2 pc = d < n ? sp[d] : make_uint2(nb, 0u);
+            kc[u] = pc.x;
+            kp[u] = (d > 0 && d <= n) ? sp[d - 1].x : 0xffffffffu;
+            q[u] = (d < n && kc[u] < nb) ? pc.y : 0u;
         }
 #pragma unroll
         for (int u = 0; u < U; u++) {
@@ -777,10 +786,9 @@ static int bin_sorted(kde_ctx* c, const double* d_x, const double* d_y, int n) {
     if (n64 > pb.cap || pb.key[0] == nullptr) {
         const int64_t cap = n64 > 1024 ? n64 : 1024;
         int rc = KDE_OK;
-        rc |= grow((void**)&pb.key[0], sizeof(uint32_t) * (cap + 4));  // + TMA tail
-        rc |= grow((void**)&pb.key[1], sizeof(uint32_t) * (cap + 4));  // + TMA tail
-        rc |= grow((void**)&pb.val[0], sizeof(uint32_t) * (cap + 4));  // + TMA tail
-        rc |= grow((void**)&pb.val[1], sizeof(uint32_t) * (cap + 4));  // + TMA tail
+        rc |= grow((void**)&pb.key[0], sizeof(uint32_t) * (cap + 4));  // + TMA tail slack
+        rc |= grow((void**)&pb.pair[0], sizeof(uint2) * (cap + 2));
+        rc |= grow((void**)&pb.pair[1], sizeof(uint2) * (cap + 2));
         rc |= grow((void**)&pb.xy, sizeof(float2) * cap);
         rc |= grow((void**)&pb.rng, sizeof(uint2) * cap);
         rc |= grow((void**)&pb.rec, sizeof(uint4) * cap);
@@ -794,7 +802,7 @@ static int bin_sorted(kde_ctx* c, const double* d_x, const double* d_y, int n) {
     uint32_t* gofs = pb.hist + kRsMaxPasses * kRsMaxDigits;
     uint32_t* bars = pb.hist + 2 * kRsMaxPasses * kRsMaxDigits;
     // the passes' CTA count: every CTA resident (cooperative launch), at most one per tile
-    const size_t dsmem = sizeof(uint32_t) * (2 * nbins + 4 * tile) + sizeof(uint16_t) * 8 * nbins;
+    const size_t dsmem = sizeof(uint2) * 2 * tile + sizeof(uint32_t) * 2 * nbins + sizeof(uint16_t) * 8 * nbins;
     auto k_first = rounds == 8 ? os_pass_kernel<8, false> : os_pass_kernel<16, false>;
     auto k_next = rounds == 8 ? os_pass_kernel<8, true> : os_pass_kernel<16, true>;
     int nsm = 148, occ0 = 0, occ1 = 0;
@@ -833,10 +841,10 @@ static int bin_sorted(kde_ctx* c, const double* d_x, const double* d_y, int n) {
         int cur = 0;
         for (int ps = 0; ps < passes; ps++) {
             OsArgs oa;
-            oa.kin = pb.key[cur];
-            oa.vin = ps == 0 ? nullptr : pb.val[cur];
-            oa.kout = pb.key[cur ^ 1];
-            oa.vout = pb.val[cur ^ 1];
+            oa.kin = ps == 0 ? pb.key[0] : nullptr;
+            oa.pin = ps == 0 ? nullptr : pb.pair[cur];
+            if (ps > 0) cur ^= 1;
+            oa.pout = pb.pair[cur];
             oa.n = n;
             oa.shift = ps * dbits;
             oa.nbins = pass_bins(ps);
@@ -852,15 +860,14 @@ static int bin_sorted(kde_ctx* c, const double* d_x, const double* d_y, int n) {
                                                                dim3(kRsThreads), args, dsmem, s);
             if (le != cudaSuccess) return cuda_fail(le, "radix pass (cooperative launch)");
             c->launches += 1;
-            cur ^= 1;
         }
-        pb.perm = pb.val[cur];
+        pb.sorted = pb.pair[cur];
         const int gg = (n + 1 + 1023) / 1024 < 148 * 8 ? (n + 1 + 1023) / 1024 : 148 * 8;
-        gather_offsets_kernel<<<gg, 256, 0, s>>>(pb.rec, pb.perm, pb.key[cur], n, nb, c->d_offsets, pb.xy, pb.rng);
+        gather_offsets_kernel<<<gg, 256, 0, s>>>(pb.rec, pb.sorted, n, nb, c->d_offsets, pb.xy, pb.rng);
         c->launches += 1;
     } else {
         cudaMemsetAsync(c->d_offsets, 0, sizeof(uint32_t) * (nb + 1), s);
-        pb.perm = pb.val[0];
+        pb.sorted = pb.pair[0];
     }
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "binning launch");

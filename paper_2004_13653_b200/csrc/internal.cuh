@@ -50,18 +50,18 @@ struct PointBufs {
     double *sy[2] = {nullptr, nullptr};
     int64_t stage_cap[2] = {0, 0};
     int stage = 0;                             // staging buffer of the next host load
-    uint32_t *key[2] = {nullptr, nullptr};     // radix ping-pong
-    uint32_t *val[2] = {nullptr, nullptr};
+    uint32_t *key[1] = {nullptr};              // keys in input order (convert)
+    uint2 *pair[2] = {nullptr, nullptr};       // radix ping-pong: (key, input position) pairs
     uint32_t *hist = nullptr;                  // radix: per-pass digit totals, their exclusive
                                                // scans, grid-barrier counters (bin.cu)
     uint32_t *ost[2] = {nullptr, nullptr};     // radix: per-CTA range histograms, their
                                                // column-wise exclusive scans [cta][digit]
     int64_t ost_cap = 0;                       // words per buffer
     uint32_t *scan_tmp = nullptr;                // band compaction: kept total
-    uint4 *rec = nullptr;                      // per input point: lx, ly, packed ranges
     float2 *xy = nullptr;                      // sorted bucket-local coordinates
     uint2 *rng = nullptr;                      // sorted packed int16 ranges
-    uint32_t *perm = nullptr;                  // sorted -> original index (alias)
+    uint4 *rec = nullptr;                      // per input point: lx, ly, packed ranges
+    uint2 *sorted = nullptr;                   // sorted (key, original index) pairs (alias)
     // banded contexts: the points binning keeps, compacted in input order before the sort
     double *cx = nullptr, *cy = nullptr;       // their coordinates
     uint32_t *cidx = nullptr;                  // their original indices
