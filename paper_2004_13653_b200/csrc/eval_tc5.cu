@@ -6,8 +6,9 @@
 // contraction S = A . B^T, A[row][p] = ky_p(row), B[col][p] = kx_p(col), both masked by the
 // point's fp64-decided integer ranges (R3).
 //
-// One CTA per SM: kW worker warps, each an independent pipeline with its OWN TMEM accumulator
-// (a 64-column slice of the SM's 512) and its own two operand buffers, plus 4 epilogue warps.
+// One CTA per SM: kW worker warps (10 when N <= 48, else 8), each an independent pipeline with
+// its OWN TMEM accumulator (a 48- or 64-column slice of the SM's 512) and its own two operand
+// buffers, plus 4 epilogue warps.
 // A worker pops (group, segment) items and walks them in BUCKET-HOMOGENEOUS chunks of 32
 // points (lane = point; a chunk's rows lie in its bucket's (B + 2F)-row window, so NA = NB =
 // (B + 2F)/8 units carry every nonzero factor); per chunk it loads the next chunk's points
@@ -17,7 +18,8 @@
 // the UMMA layouts (A: MN-major 128-byte swizzle; B: MN-major unswizzled), and one elected
 // lane issues its two tcgen05.mma.kind::f16 (M = 128, N, K = 16) -- no CTA barrier and no
 // cross-warp ordering: the workers never wait on each other.  At an item's end the worker
-// commits its accumulator and posts a drain request; the 4 epilogue warps (TMEM lanes
+// commits its accumulator and posts a drain request (a ready bit per epilogue warp + an
+// mbarrier doorbell the idle epilogue warps sleep on); the 4 epilogue warps (TMEM lanes
 // 32e..32e+31 each) read it with tcgen05.ld into the item's splat slot and release it.
 // Per (item, pixel) the accumulation order is the item's chunk order (deterministic); the
 // combine pass sums the slots in a fixed order (bitwise sharding).
@@ -31,14 +33,14 @@
 namespace kde {
 namespace tc5 {
 
-constexpr int kW = 8;                      // worker warps per CTA (one CTA per SM)
+// worker warps per CTA (one CTA per SM): as many 48- or 64-column accumulators as the SM's 512
+// TMEM columns hold (10 for N <= 48, 8 for N = 64)
+template <int N> struct Workers { static constexpr int kW = N <= 48 ? 10 : 8, kAcc = N <= 48 ? 48 : 64; };
 constexpr int kEpi = 4;                    // epilogue warps
-constexpr int kThreads = 32 * (kW + kEpi);
 constexpr int kPts = 32;                   // points per chunk (K of two MMAs)
 constexpr int kABytes = kTcM * kPts * 2;   // A: 128 rows x 32 fp16
 constexpr uint32_t kALBO = 4096;           // A: bytes between the two 64-row atoms
 constexpr int kSBO = 512;                  // B: bytes between 8-column core-matrix groups
-constexpr int kAccCols = 64;               // TMEM columns per worker accumulator (N <= 64)
 
 struct Args {
     Geom g;
@@ -106,6 +108,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         if (ok) return;
         if (++n > (1u << 26)) __trap();
     }
+}
+
+// one bounded wait: true once the phase of the given parity has completed; otherwise the
+// thread is suspended for up to ~ns nanoseconds (a doorbell that does not spin)
+__device__ __forceinline__ bool mbar_try_wait_ns(uint64_t* bar, uint32_t parity, uint32_t ns) {
+    uint32_t ok = 0;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
+        : "memory");
+    return ok != 0;
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -205,6 +223,10 @@ __device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {  // packed f
     return r;
 }
 
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+    return make_uint4(pack_half2(f[0], f[1]), pack_half2(f[2], f[3]), pack_half2(f[4], f[5]), pack_half2(f[6], f[7]));
+}
+
 // 8 factors -> masked to [lo, lo + span] (relative to c0) -> fp16 x 8
 __device__ __forceinline__ uint4 mask_pack(float (&f)[8], int c0, int lo, int span) {
     const int l0 = max(lo - c0, 0), h0 = min(lo + span - c0, 7);
@@ -254,14 +276,20 @@ __device__ __forceinline__ void factors2(float d0, float d1, const Args& a, floa
 
 
 
-template <int K, bool REC, int NU>
-__global__ void __launch_bounds__(kThreads, 1) tc5_kernel(const Args a) {
+template <int K, bool REC, int NU, int NC>
+__global__ void __launch_bounds__(32 * (Workers<NC>::kW + kEpi), 1) tc5_kernel(const Args a) {
+    constexpr int kW = Workers<NC>::kW, kAccCols = Workers<NC>::kAcc, kThreads = 32 * (kW + kEpi);
     extern __shared__ __align__(1024) char smem[];
     __shared__ __align__(8) uint64_t bar_buf[kW][2];    // MMAs done reading worker w's buffer b
     __shared__ __align__(8) uint64_t bar_acc[kW];       // worker w's accumulator complete
     __shared__ __align__(8) uint64_t bar_drained[kW];   // ... read back by the 4 epilogue warps
     __shared__ int s_slot[kW];                          // the posted item's splat slot
-    __shared__ volatile int s_post[kW];                 // items posted by worker w (-1 - k: done)
+    __shared__ unsigned s_ready[kEpi];                  // bit w: worker w's posted item not yet
+                                                        // drained by epilogue warp e
+    __shared__ unsigned s_fin;                          // bit w: worker w has no more items
+    __shared__ __align__(8) uint64_t bar_post[kEpi];    // doorbell of epilogue warp e (a post or a
+                                                        // finish arrives; phases may merge: the
+                                                        // waits are bounded and re-check s_ready)
     __shared__ uint32_t s_tmem;
 
     const Geom& g = a.g;
@@ -279,8 +307,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc5_kernel(const Args a) {
             mbar_init(&bar_buf[w][1], 1);
             mbar_init(&bar_acc[w], 1);
             mbar_init(&bar_drained[w], kEpi);
-            s_post[w] = 0;
         }
+        for (int e = 0; e < kEpi; e++) {
+            s_ready[e] = 0u;
+            mbar_init(&bar_post[e], 1);
+        }
+        s_fin = 0u;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     for (int e = t; e < kW * 2 * a.buf_bytes / 16; e += kThreads) sts128(sm0 + 16u * e, make_uint4(0u, 0u, 0u, 0u));
@@ -381,7 +413,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc5_kernel(const Args a) {
                 }
                 if (bf) prev_ua[1] = ua0;
                 else prev_ua[0] = ua0;
-                // the NA row units and NB column units of this chunk, straight-line
+                // the NA row units and NB column units of this chunk, straight-line.  When all 32
+                // points' ranges cover units 1 .. NU-2 on both axes (a full chunk away from the
+                // raster edges: the usual case), those units need no mask.
+                const bool inner = __all_sync(0xffffffffu, jlo <= (ua0 + 1) * 8 && jlo + jsp >= (ua0 + NU - 1) * 8 - 1 &&
+                                                               ilo <= 8 && ilo + isp >= (NU - 1) * 8 - 1);
 #pragma unroll
                 for (int k = 0; k < NU; k++) {
                     float fa[8], fb[8];
@@ -392,8 +428,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc5_kernel(const Args a) {
                         factors<K, REC>(da, a, fa);
                         factors<K, REC>(db, a, fb);
                     }
-                    sts128(a_unit_addr(ab, ua0 + k, r8, kALBO), mask_pack(fa, (ua0 + k) * 8, jlo, jsp));
-                    sts128(bb + k * kSBO, mask_pack(fb, k * 8, ilo, isp));
+                    if (k >= 1 && k <= NU - 2 && inner) {
+                        sts128(a_unit_addr(ab, ua0 + k, r8, kALBO), pack8(fa));
+                        sts128(bb + k * kSBO, pack8(fb));
+                    } else {
+                        sts128(a_unit_addr(ab, ua0 + k, r8, kALBO), mask_pack(fa, (ua0 + k) * 8, jlo, jsp));
+                        sts128(bb + k * kSBO, mask_pack(fb, k * 8, ilo, isp));
+                    }
                 }
                 fence_async_smem();
                 __syncwarp();
@@ -414,56 +455,64 @@ __global__ void __launch_bounds__(kThreads, 1) tc5_kernel(const Args a) {
             if (lane == 0) {  // the item's accumulator completes on bar_acc[w]: post it
                 s_slot[w] = it.w;
                 __threadfence_block();
-                s_post[w] = nitem + 1;
+#pragma unroll
+                for (int e = 0; e < kEpi; e++) atomicOr(&s_ready[e], 1u << w);
+#pragma unroll
+                for (int e = 0; e < kEpi; e++) mbar_arrive(&bar_post[e]);
             }
             nitem++;
         }
         if (lane == 0) {
             if (q) atomicAdd(&a.totals[kTotChunksExec], q);  // executed chunks (kde_stats.tc_mma_flops)
             __threadfence_block();
-            s_post[w] = -1 - nitem;  // done after nitem items
+            atomicOr(&s_fin, 1u << w);  // (after its last post)
+#pragma unroll
+            for (int e = 0; e < kEpi; e++) mbar_arrive(&bar_post[e]);
         }
     } else {
         // ------------------------------------------------------------------ epilogue
         const int quad = warp & 3;  // tcgen05.ld: warp reaches TMEM lanes 32 (warp % 4) .. + 31
         const int row = quad * 32 + lane;
         const int slot_floats = pg.slot_w * pg.slot_h;
-        int done[kW];
-#pragma unroll
-        for (int w = 0; w < kW; w++) done[w] = 0;
-        int finished = 0;
-        while (finished < kW) {
-            bool any = false;
-            finished = 0;
-#pragma unroll
-            for (int w = 0; w < kW; w++) {
-                const int pv = s_post[w];
-                const int posted = pv >= 0 ? pv : -1 - pv;
-                if (pv < 0 && done[w] == posted) {
-                    finished++;
-                    continue;
-                }
-                if (done[w] < posted) {
-                    mbar_wait(&bar_acc[w], (uint32_t)done[w] & 1u);
-                    tc_fence_after();
-                    const int slot = s_slot[w];
-                    float* dst = a.splat + (size_t)slot * slot_floats + (size_t)row * pg.slot_w;
-                    for (int c0 = 0; c0 < a.n; c0 += 16) {
-                        float v[16];
-                        tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(w * kAccCols + c0), v);
-#pragma unroll
-                        for (int k = 0; k < 16; k += 4)
-                            if (c0 + k < pg.slot_w)
-                                *reinterpret_cast<float4*>(dst + c0 + k) = make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]);
-                    }
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&bar_drained[w]);
-                    done[w]++;
-                    any = true;
-                }
+        const int e = warp - kW;  // this epilogue warp's ready word
+        volatile unsigned* ready = &s_ready[e];
+        volatile unsigned* fin = &s_fin;
+        uint32_t par = 0;   // bit w: parity of worker w's next accumulator phase
+        uint32_t bell = 0;  // parity of the doorbell's next phase
+        for (;;) {
+            unsigned m = __shfl_sync(0xffffffffu, *ready, 0);  // warp-uniform (tcgen05.ld is .aligned)
+            if (m == 0u) {  // nothing posted: done when every worker is, else sleep on the doorbell
+                const unsigned f = __shfl_sync(0xffffffffu, *fin, 0);
+                __threadfence_block();
+                if (f == (1u << kW) - 1u && __shfl_sync(0xffffffffu, *ready, 0) == 0u) break;
+                if (mbar_try_wait_ns(&bar_post[e], bell, 2000u)) bell ^= 1u;
+                __syncwarp();
+                continue;
             }
-            if (!any) __nanosleep(200);
+            while (m) {
+                const int w = __ffs(m) - 1;
+                m &= m - 1;
+                mbar_wait(&bar_acc[w], (par >> w) & 1u);
+                par ^= 1u << w;
+                tc_fence_after();
+                const int slot = s_slot[w];
+                float* dst = a.splat + (size_t)slot * slot_floats + (size_t)row * pg.slot_w;
+                for (int c0 = 0; c0 < a.n; c0 += 16) {
+                    float v[16];
+                    tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(w * kAccCols + c0), v);
+#pragma unroll
+                    for (int k = 0; k < 16; k += 4)
+                        if (c0 + k < pg.slot_w)
+                            *reinterpret_cast<float4*>(dst + c0 + k) = make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    atomicAnd(&s_ready[e], ~(1u << w));  // before the release: the next post sets it again
+                    mbar_arrive(&bar_drained[w]);
+                }
+                __syncwarp();
+            }
         }
     }
     tc_fence_before();
@@ -474,11 +523,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc5_kernel(const Args a) {
     }
 }
 
-template <int K, bool REC, int NU>
+template <int K, bool REC, int NU, int NC>
 static int launch(kde_ctx* c, EvalPlan& pl, Args& a, cudaStream_t s) {
     a.buf_bytes = kABytes + a.n * kPts * 2;
-    const size_t smem = (size_t)kW * 2 * a.buf_bytes + 1024;
-    auto kern = tc5_kernel<K, REC, NU>;
+    const size_t smem = (size_t)Workers<NC>::kW * 2 * a.buf_bytes + 1024;
+    auto kern = tc5_kernel<K, REC, NU, NC>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cuda_fail(e, "tensor-core kernel attribute");
     int nsm = 148;
@@ -487,20 +536,20 @@ static int launch(kde_ctx* c, EvalPlan& pl, Args& a, cudaStream_t s) {
         fprintf(stderr, "[kde] tc5: NU=%d smem=%zu grid=%d n=%d\n", NU, smem, nsm, a.n);
     cudaMemsetAsync(pl.d_totals + kTotQueue, 0, sizeof(int), s);  // work-queue head
     tmark(c, 3, s);
-    kern<<<nsm, kThreads, smem, s>>>(a);  // persistent: one CTA per SM
+    kern<<<nsm, 32 * (Workers<NC>::kW + kEpi), smem, s>>>(a);  // persistent: one CTA per SM
     return KDE_OK;
 }
 
 template <int K, bool REC>
 static int launch_nu(kde_ctx* c, EvalPlan& pl, Args& a, cudaStream_t s, int nu) {
-    switch (nu) {
-    case 2: return launch<K, REC, 2>(c, pl, a, s);
-    case 3: return launch<K, REC, 3>(c, pl, a, s);
-    case 4: return launch<K, REC, 4>(c, pl, a, s);
-    case 5: return launch<K, REC, 5>(c, pl, a, s);
-    case 6: return launch<K, REC, 6>(c, pl, a, s);
-    case 7: return launch<K, REC, 7>(c, pl, a, s);
-    default: return launch<K, REC, 8>(c, pl, a, s);
+    switch (nu) {  // N = window rounded up to 16: <= 48 up to 6 units (10 workers), else 64 (8)
+    case 2: return launch<K, REC, 2, 48>(c, pl, a, s);
+    case 3: return launch<K, REC, 3, 48>(c, pl, a, s);
+    case 4: return launch<K, REC, 4, 48>(c, pl, a, s);
+    case 5: return launch<K, REC, 5, 48>(c, pl, a, s);
+    case 6: return launch<K, REC, 6, 48>(c, pl, a, s);
+    case 7: return launch<K, REC, 7, 64>(c, pl, a, s);
+    default: return launch<K, REC, 8, 64>(c, pl, a, s);
     }
 }
 
@@ -516,7 +565,7 @@ int launch_tc5(kde_ctx* c, cudaStream_t s) {
     if (env && atoi(env) == 0) return KDE_EUNSUPPORTED;
     const int win = c->g.B + 2 * c->g.F;
     const int nu = (win + 7) / 8;
-    if (pg.nsub() != 1 || c->g.B % 8 != 0 || pg.mma_n > tc5::kAccCols || nu < 2 || nu > 8 || nu * 8 > pg.mma_n)
+    if (pg.nsub() != 1 || c->g.B % 8 != 0 || pg.mma_n > 64 || (nu <= 6 && pg.mma_n > 48) || nu < 2 || nu > 8 || nu * 8 > pg.mma_n)
         return KDE_EUNSUPPORTED;
     tc5::Args a;
     a.g = c->g;
