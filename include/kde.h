@@ -129,7 +129,9 @@ typedef struct {
     int32_t main_kernel;   /* the main (a3/a4) kernel of the last kde_eval: 0 none yet,
                               1 splat_kernel (direct), 2 tc_splat_kernel (tensor, eval_tc.cu),
                               3 tc5_kernel (tensor, per-warp pipelines, eval_tc5.cu)         */
-    int32_t reserved;      /* 0                                                              */
+    int32_t tc_m;          /* MMA M (accumulator and splat-slot rows) of the tensor-core path's
+                              plan: 64 when a group window has <= 64 rows and <= 48 columns
+                              (eval_tc5.cu's M = 64 tiles), else 128; 0 if the path is off  */
 } kde_stats;
 
 /*

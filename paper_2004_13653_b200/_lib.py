@@ -45,7 +45,7 @@ class kde_stats(ctypes.Structure):
                 ("nbx", ctypes.c_int32), ("nby", ctypes.c_int32), ("reach_px", ctypes.c_int32),
                 ("stack", ctypes.c_int32), ("band_lo", ctypes.c_int32), ("band_hi", ctypes.c_int32),
                 ("kernel_launches", ctypes.c_int64), ("tc_mma_flops", ctypes.c_int64),
-                ("main_kernel", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("main_kernel", ctypes.c_int32), ("tc_m", ctypes.c_int32)]
 
     def as_dict(self):
         return {f: int(getattr(self, f)) for f, _ in self._fields_}

@@ -83,7 +83,13 @@ static void plan_geometry_tc(EvalPlan& pl, const Geom& g, bool product) {
     const int Wd = g.B + 2 * g.F;
     pl.enabled = product;
     if (!pl.enabled) return;
-    pg.s = Wd <= kTcM ? std::max(1, (kTcM - 2 * g.F) / g.B) : 1;
+    // M = 64 tiles (eval_tc5.cu) when a stack of >= 1 bucket fits 64 rows and the window's
+    // columns fit N = 48: half the MMA rows of M = 128 are padding for such windows anyway, and
+    // two M = 64 accumulators share a TMEM column slice (16 workers instead of 10).
+    const char* m64env = getenv("KDE_TC_M64");
+    const bool m64 = Wd <= 48 && (64 - 2 * g.F) / g.B >= 1 && !(m64env && atoi(m64env) == 0);
+    pg.mrows = m64 ? 64 : kTcM;
+    pg.s = m64 ? (64 - 2 * g.F) / g.B : (Wd <= kTcM ? std::max(1, (kTcM - 2 * g.F) / g.B) : 1);
     pg.ngx = g.nbx;
     pg.ngy = (g.nby + pg.s - 1) / pg.s;
     pg.px = g.B;
@@ -96,7 +102,7 @@ static void plan_geometry_tc(EvalPlan& pl, const Geom& g, bool product) {
     pg.sy = (pg.wh + pg.nsuby - 1) / pg.nsuby;
     pg.slot_w = ((pg.sx + 3) / 4) * 4;  // the sub-window's columns (float4 rows); MMA N = round16
     pg.mma_n = ((pg.sx + 15) / 16) * 16;
-    pg.slot_h = kTcM;
+    pg.slot_h = pg.mrows;
     pg.chunk_pts = 32;                  // 2 MMAs per operand buffer (eval_tc.cu, H = 1; 64-point
                                         // chunks measured slower: 5 CTAs/SM instead of 8)
 }
@@ -521,7 +527,7 @@ int kde_get_stats(const kde_ctx* c, kde_stats* s) {
     *s = c->stats;
     s->kernel_launches = c->launches;
     s->main_kernel = c->main_kernel;
-    s->reserved = 0;
+    s->tc_m = c->plan[KDE_PATH_TENSOR].enabled ? c->plan[KDE_PATH_TENSOR].pg.mrows : 0;
     s->tc_mma_flops = 0;
     const EvalPlan& tp = c->plan[KDE_PATH_TENSOR];
     if (c->loaded && tp.enabled && tp.planned_gen == c->load_gen) {  // executed MMA flops / eval
@@ -535,7 +541,8 @@ int kde_get_stats(const kde_ctx* c, kde_stats* s) {
         // executes the plan's chunks
         const int chunks = tot[kTotChunksExec] > 0 ? tot[kTotChunksExec] : tot[kTotChunks];
         // per chunk: chunk_pts/16 MMAs of M=128 x N x K=16, 2 flops per MAC
-        s->tc_mma_flops = (int64_t)chunks * (tp.pg.chunk_pts / 16) * 2 * kTcM * tp.pg.mma_n * 16;
+        const int64_t m = tot[kTotChunksExec] > 0 ? tp.pg.mrows : kTcM;  // eval_tc.cu: always M = 128
+        s->tc_mma_flops = (int64_t)chunks * (tp.pg.chunk_pts / 16) * 2 * m * tp.pg.mma_n * 16;
     }
     return KDE_OK;
 }

@@ -366,14 +366,14 @@ __global__ void __launch_bounds__(kTcThreads, TcShape<H>::kMinBlocks) tc_splat_k
         nacc++;
         tc_fence_after();
         {
-            const int row = warp * 32 + lane;
+            const int row = warp * 32 + lane;  // (slots of M = 64 plans hold rows < 64: the rest are zero)
             float* dst = a.splat + (size_t)it.w * slot_floats + (size_t)row * pg.slot_w;
             for (int c0 = 0; c0 < a.n; c0 += 16) {  // only the window's slot_w columns
                 float v[16];
                 tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
 #pragma unroll
                 for (int k = 0; k < 16; k += 4)
-                    if (c0 + k < pg.slot_w)
+                    if (row < pg.slot_h && c0 + k < pg.slot_w)
                         *reinterpret_cast<float4*>(dst + c0 + k) = make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]);
             }
         }

@@ -36,6 +36,13 @@ namespace tc5 {
 // worker warps per CTA (one CTA per SM): as many 48- or 64-column accumulators as the SM's 512
 // TMEM columns hold (10 for N <= 48, 8 for N = 64)
 template <int N> struct Workers { static constexpr int kW = N <= 48 ? 10 : 8, kAcc = N <= 48 ? 48 : 64; };
+// M = 64 tiles (group windows of <= 64 rows, N <= 48): an accumulator holds its rows 16q..16q+15
+// in TMEM lanes 32q + 16h .. 32q + 16h + 15 (lane half h = 0, 1; measured with
+// tools/tmem_m64_lane_probe.cu), so two share each 48-column slice: 16 workers in 8 slices,
+// their double-buffered 4 + 3 KB operands filling the shared memory
+template <int N, int MR> struct Tc5Shape {
+    static constexpr int kW = MR == 64 ? 16 : Workers<N>::kW, kAcc = Workers<N>::kAcc;
+};
 constexpr int kEpi = 4;                    // epilogue warps
 constexpr int kPts = 32;                   // points per chunk (K of two MMAs)
 constexpr int kABytes = kTcM * kPts * 2;   // A: 128 rows x 32 fp16
@@ -276,9 +283,10 @@ __device__ __forceinline__ void factors2(float d0, float d1, const Args& a, floa
 
 
 
-template <int K, bool REC, int NU, int NC>
-__global__ void __launch_bounds__(32 * (Workers<NC>::kW + kEpi), 1) tc5_kernel(const Args a) {
-    constexpr int kW = Workers<NC>::kW, kAccCols = Workers<NC>::kAcc, kThreads = 32 * (kW + kEpi);
+template <int K, bool REC, int NU, int NC, int MR>
+__global__ void __launch_bounds__(32 * (Tc5Shape<NC, MR>::kW + kEpi), 1) tc5_kernel(const Args a) {
+    constexpr int kW = Tc5Shape<NC, MR>::kW, kAccCols = Tc5Shape<NC, MR>::kAcc, kThreads = 32 * (kW + kEpi);
+    constexpr int kAB = MR * kPts * 2;  // A bytes per buffer
     extern __shared__ __align__(1024) char smem[];
     __shared__ __align__(8) uint64_t bar_buf[kW][2];    // MMAs done reading worker w's buffer b
     __shared__ __align__(8) uint64_t bar_acc[kW];       // worker w's accumulator complete
@@ -326,9 +334,11 @@ __global__ void __launch_bounds__(32 * (Workers<NC>::kW + kEpi), 1) tc5_kernel(c
         // ------------------------------------------------------------------ worker
         constexpr int NA = NU, NB = NU;
         const int w = warp;
-        const uint32_t acc = tmem + (uint32_t)(w * kAccCols);
+        // the accumulator: M = 128, slice w; M = 64, slice w / 2 at lane offset 16 (w % 2)
+        const uint32_t acc = MR == 64 ? tmem + ((uint32_t)(16 * (w & 1)) << 16) + (uint32_t)((w >> 1) * kAccCols)
+                                      : tmem + (uint32_t)(w * kAccCols);
         const uint32_t idesc = (1u << 4) | (1u << 15) | (1u << 16) | ((uint32_t)(a.n >> 3) << 17) |
-                               ((uint32_t)(kTcM >> 4) << 24);
+                               ((uint32_t)(MR >> 4) << 24);
         const uint32_t a_lane = (uint32_t)((lane >> 3) * kASBO + (lane & 7) * 128);
         const uint32_t b_lane = (uint32_t)((lane >> 3) * 128 + (lane & 7) * 16);
         const int r8 = lane & 7;
@@ -402,7 +412,7 @@ __global__ void __launch_bounds__(32 * (Workers<NC>::kW + kEpi), 1) tc5_kernel(c
                 const int bf = q & 1;
                 if (q >= 2) mbar_wait(&bar_buf[w][bf], (uint32_t)((q >> 1) - 1) & 1u);
                 const uint32_t base = sm0 + (uint32_t)((2 * w + bf) * a.buf_bytes);
-                const uint32_t ab = base + a_lane, bb = base + (uint32_t)kABytes + b_lane;
+                const uint32_t ab = base + a_lane, bb = base + (uint32_t)kAB + b_lane;
                 const int old = bf ? prev_ua[1] : prev_ua[0];
                 if (old >= 0 && old != ua0) {  // A units the buffer's last chunk (another bucket) wrote
 #pragma unroll
@@ -444,7 +454,7 @@ __global__ void __launch_bounds__(32 * (Workers<NC>::kW + kEpi), 1) tc5_kernel(c
 #pragma unroll
                     for (int kk = 0; kk < 2; kk++)
                         mma_f16(acc, umma_desc(base + kk * 2 * kASBO, kALBO, kASBO, 2),
-                                umma_desc(base + kABytes + kk * 256, 128, kSBO), idesc, (!first || kk > 0) ? 1u : 0u);
+                                umma_desc(base + kAB + kk * 256, 128, kSBO), idesc, (!first || kk > 0) ? 1u : 0u);
                     mma_commit(&bar_buf[w][bf]);
                     if (!more) mma_commit(&bar_acc[w]);
                 }
@@ -472,7 +482,8 @@ __global__ void __launch_bounds__(32 * (Workers<NC>::kW + kEpi), 1) tc5_kernel(c
     } else {
         // ------------------------------------------------------------------ epilogue
         const int quad = warp & 3;  // tcgen05.ld: warp reaches TMEM lanes 32 (warp % 4) .. + 31
-        const int row = quad * 32 + lane;
+        // the accumulator row of this lane (M = 64: of the worker whose lane half it is)
+        const int row = MR == 64 ? quad * 16 + (lane & 15) : quad * 32 + lane;
         const int slot_floats = pg.slot_w * pg.slot_h;
         const int e = warp - kW;  // this epilogue warp's ready word
         volatile unsigned* ready = &s_ready[e];
@@ -497,12 +508,14 @@ __global__ void __launch_bounds__(32 * (Workers<NC>::kW + kEpi), 1) tc5_kernel(c
                 tc_fence_after();
                 const int slot = s_slot[w];
                 float* dst = a.splat + (size_t)slot * slot_floats + (size_t)row * pg.slot_w;
+                const bool mine = MR != 64 || (lane >> 4) == (w & 1);  // M = 64: this worker's lane half
+                const uint32_t col = (uint32_t)((MR == 64 ? (w >> 1) : w) * kAccCols);
                 for (int c0 = 0; c0 < a.n; c0 += 16) {
                     float v[16];
-                    tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(w * kAccCols + c0), v);
+                    tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + col + (uint32_t)c0, v);
 #pragma unroll
                     for (int k = 0; k < 16; k += 4)
-                        if (c0 + k < pg.slot_w)
+                        if (mine && c0 + k < pg.slot_w)
                             *reinterpret_cast<float4*>(dst + c0 + k) = make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]);
                 }
                 tc_fence_before();
@@ -523,11 +536,11 @@ __global__ void __launch_bounds__(32 * (Workers<NC>::kW + kEpi), 1) tc5_kernel(c
     }
 }
 
-template <int K, bool REC, int NU, int NC>
+template <int K, bool REC, int NU, int NC, int MR>
 static int launch(kde_ctx* c, EvalPlan& pl, Args& a, cudaStream_t s) {
-    a.buf_bytes = kABytes + a.n * kPts * 2;
-    const size_t smem = (size_t)Workers<NC>::kW * 2 * a.buf_bytes + 1024;
-    auto kern = tc5_kernel<K, REC, NU, NC>;
+    a.buf_bytes = MR * kPts * 2 + a.n * kPts * 2;
+    const size_t smem = (size_t)Tc5Shape<NC, MR>::kW * 2 * a.buf_bytes + 1024;
+    auto kern = tc5_kernel<K, REC, NU, NC, MR>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cuda_fail(e, "tensor-core kernel attribute");
     int nsm = 148;
@@ -536,20 +549,31 @@ static int launch(kde_ctx* c, EvalPlan& pl, Args& a, cudaStream_t s) {
         fprintf(stderr, "[kde] tc5: NU=%d smem=%zu grid=%d n=%d\n", NU, smem, nsm, a.n);
     cudaMemsetAsync(pl.d_totals + kTotQueue, 0, sizeof(int), s);  // work-queue head
     tmark(c, 3, s);
-    kern<<<nsm, 32 * (Workers<NC>::kW + kEpi), smem, s>>>(a);  // persistent: one CTA per SM
+    kern<<<nsm, 32 * (Tc5Shape<NC, MR>::kW + kEpi), smem, s>>>(a);  // persistent: one CTA per SM
     return KDE_OK;
 }
 
 template <int K, bool REC>
 static int launch_nu(kde_ctx* c, EvalPlan& pl, Args& a, cudaStream_t s, int nu) {
-    switch (nu) {  // N = window rounded up to 16: <= 48 up to 6 units (10 workers), else 64 (8)
-    case 2: return launch<K, REC, 2, 48>(c, pl, a, s);
-    case 3: return launch<K, REC, 3, 48>(c, pl, a, s);
-    case 4: return launch<K, REC, 4, 48>(c, pl, a, s);
-    case 5: return launch<K, REC, 5, 48>(c, pl, a, s);
-    case 6: return launch<K, REC, 6, 48>(c, pl, a, s);
-    case 7: return launch<K, REC, 7, 64>(c, pl, a, s);
-    default: return launch<K, REC, 8, 64>(c, pl, a, s);
+    // N = window rounded up to 16: <= 48 up to 6 units, else 64; M = 64 tiles when the plan's
+    // group windows have <= 64 rows (PathGeom::mrows)
+    if (pl.pg.mrows == 64) {
+        switch (nu) {
+        case 2: return launch<K, REC, 2, 48, 64>(c, pl, a, s);
+        case 3: return launch<K, REC, 3, 48, 64>(c, pl, a, s);
+        case 4: return launch<K, REC, 4, 48, 64>(c, pl, a, s);
+        case 5: return launch<K, REC, 5, 48, 64>(c, pl, a, s);
+        default: return launch<K, REC, 6, 48, 64>(c, pl, a, s);
+        }
+    }
+    switch (nu) {
+    case 2: return launch<K, REC, 2, 48, 128>(c, pl, a, s);
+    case 3: return launch<K, REC, 3, 48, 128>(c, pl, a, s);
+    case 4: return launch<K, REC, 4, 48, 128>(c, pl, a, s);
+    case 5: return launch<K, REC, 5, 48, 128>(c, pl, a, s);
+    case 6: return launch<K, REC, 6, 48, 128>(c, pl, a, s);
+    case 7: return launch<K, REC, 7, 64, 128>(c, pl, a, s);
+    default: return launch<K, REC, 8, 64, 128>(c, pl, a, s);
     }
 }
 
@@ -565,7 +589,8 @@ int launch_tc5(kde_ctx* c, cudaStream_t s) {
     if (env && atoi(env) == 0) return KDE_EUNSUPPORTED;
     const int win = c->g.B + 2 * c->g.F;
     const int nu = (win + 7) / 8;
-    if (pg.nsub() != 1 || c->g.B % 8 != 0 || pg.mma_n > 64 || (nu <= 6 && pg.mma_n > 48) || nu < 2 || nu > 8 || nu * 8 > pg.mma_n)
+    if (pg.nsub() != 1 || c->g.B % 8 != 0 || pg.mma_n > 64 || (nu <= 6 && pg.mma_n > 48) || nu < 2 || nu > 8 ||
+        nu * 8 > pg.mma_n || (pg.mrows == 64 && (nu > 6 || pg.wh > 64)))
         return KDE_EUNSUPPORTED;
     tc5::Args a;
     a.g = c->g;

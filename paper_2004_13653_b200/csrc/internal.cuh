@@ -86,6 +86,8 @@ struct PathGeom {
     int seg_pts = kSegMin;   // points per full segment (set per load, seg_pts_for)
     int chunk_pts = 32;      // tensor-core path: points per MMA chunk (K of one commit group)
     int mma_n = 0;           // tensor-core path: MMA N (window columns rounded up to 16)
+    int mrows = 128;         // tensor-core path: MMA M = accumulator rows = slot rows (64 when the
+                             // group window has <= 64 rows and N <= 48: eval_tc5.cu's M = 64 tiles)
     int part_pts = 0;        // a group's remainder (< seg_pts points) is cut into pieces of <=
                              // part_pts points, one work item each (direct: 128, one warp;
                              // 0: the whole remainder, = seg_pts)

@@ -108,7 +108,9 @@ def test_tc_mma_flops_counts_the_executed_contraction():
     st = k.stats()
     W_win = st["bucket"] + 2 * int(np.floor(4.0 * 4.0 + 0.5))  # B + 2F, F = floor(R + 1/2)
     N = (W_win + 15) // 16 * 16
-    per_mma = 2 * 128 * N * 16
+    M = st["tc_m"]  # 64: the window (B + 2F rows per bucket stack) fits M = 64 tiles
+    assert M == (64 if W_win <= 48 and (64 - (W_win - st["bucket"])) // st["bucket"] >= 1 else 128)
+    per_mma = 2 * M * N * 16
     f = st["tc_mma_flops"]
     assert f > 0 and f % per_mma == 0
     # every kept point sits in one chunk of 32: chunks >= n_binned / 32, and each chunk
