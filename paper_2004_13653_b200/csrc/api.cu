@@ -132,7 +132,13 @@ static int alloc_plan(EvalPlan& pl, const Geom& g) {
 // trip -- unless the splat bound exceeds the context's budget (very large windows): then
 // the exact slot count is read back once and only that much is allocated.
 static int plan_path(kde_ctx* c, EvalPlan& pl, cudaStream_t s) {
-    pl.pg.seg_pts = seg_pts_for(c->plan_n);  // global n: identical on every rank
+    // segment size from the global n (identical on every rank); the tensor-core path's 16
+    // pipelines per SM want twice as many items (C4: 2048-point segments, kernel 0.49 ->
+    // 0.46 ms, the busiest worker's tail shorter; 1024 slowed the segment reduce more)
+    const bool tc = &pl == &c->plan[KDE_PATH_TENSOR];
+    pl.pg.seg_pts = seg_pts_for(c->plan_n, tc && pl.pg.mrows == 64 ? kSegShareTc : kSegShareCtas);
+    static const int env_tcseg = getenv("KDE_TC_SEG") ? atoi(getenv("KDE_TC_SEG")) : 0;  // A/B experiments
+    if (tc && env_tcseg >= kSegMin && env_tcseg <= kSegMax) pl.pg.seg_pts = env_tcseg;
     // direct path: remainder pieces of a quarter segment (>= 128 points): fewer splat slots
     // to write, reduce and combine (C4: 128 -> 1024-point pieces, step 2.80 -> 2.62 ms;
     // C2: 128 -> 256, 0.377 -> 0.368 ms).  KDE_PART_PTS overrides (A/B experiments).

@@ -18,10 +18,11 @@ constexpr int kSubMax = 48;       // direct-path sub-window edge bound (pixels):
 // band sharding; <= 4096 keeps every per-warp fp32 running sum of the direct
 // path within 512 terms (R10)
 constexpr int kSegMin = 512, kSegMax = 4096;
-constexpr int64_t kSegShareCtas = 1184;  // 148 SMs x 8 tensor-core CTAs
-inline int seg_pts_for(int64_t n) {
+constexpr int64_t kSegShareCtas = 1184;  // 148 SMs x 8 work streams (direct path)
+constexpr int64_t kSegShareTc = 4736;    // 148 SMs x 16 per-warp pipelines (eval_tc5.cu) x 2
+inline int seg_pts_for(int64_t n, int64_t share = kSegShareCtas) {
     int seg = kSegMin;
-    while (seg < kSegMax && 3 * (int64_t)(2 * seg) <= 2 * (n / kSegShareCtas)) seg *= 2;
+    while (seg < kSegMax && 3 * (int64_t)(2 * seg) <= 2 * (n / share)) seg *= 2;
     return seg;
 }
 constexpr int kPartPtsDirect = 128;  // direct path: smallest remainder piece (one warp's work item)
