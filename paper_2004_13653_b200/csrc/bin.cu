@@ -115,8 +115,9 @@ __global__ void __launch_bounds__(kRsThreads, 4) bin_convert_kernel(
     uint32_t* __restrict__ key, uint4* __restrict__ rec, unsigned long long* __restrict__ stats, int passes,
     int dbits, uint32_t* __restrict__ ghist, int tile, int ntiles, uint32_t* __restrict__ rowhist0, int nbins0,
     int split) {
-    __shared__ uint32_t h[kRsMaxPasses * kRsMaxDigits];
-    for (int d = threadIdx.x; d < passes * kRsMaxDigits; d += kRsThreads) h[d] = 0;
+    constexpr int hpasses = 1;  // the first pass's digit totals (later passes total their own columns)
+    __shared__ uint32_t h[kRsMaxDigits];
+    for (int d = threadIdx.x; d < hpasses * kRsMaxDigits; d += kRsThreads) h[d] = 0;
     unsigned long long nf = 0, no = 0, up = 0;
     const int rb = g.rb, re = g.re;
     const uint32_t lmask = (1u << dbits) - 1u;
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(kRsThreads, 4) bin_convert_kernel(
             rec[i] = make_uint4(__float_as_uint(b.lx), __float_as_uint(b.ly),
                                 ((uint32_t)b.ilo & 0xffffu) | ((uint32_t)b.ihi << 16),
                                 ((uint32_t)b.jlo & 0xffffu) | ((uint32_t)b.jhi << 16));
-            for (int ps = 0; ps < passes; ps++) {
+            for (int ps = 0; ps < hpasses; ps++) {
                 const uint32_t dg = b.key >> (ps * dbits);
                 atomicAdd(&h[ps * kRsMaxDigits + (ps == passes - 1 ? dg : dg & lmask)], 1u);
             }
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(kRsThreads, 4) bin_convert_kernel(
         for (int k = 0; k < kRsThreads / 32; k++) t += s[threadIdx.x][k];
         if (t) atomicAdd(&stats[threadIdx.x], t);
     }
-    for (int d = threadIdx.x; d < passes * kRsMaxDigits; d += kRsThreads)
+    for (int d = threadIdx.x; d < hpasses * kRsMaxDigits; d += kRsThreads)
         if (h[d]) atomicAdd(&ghist[d], h[d]);
     for (int d = threadIdx.x; d < nbins0; d += kRsThreads)  // the first pass's range histogram
         if (h[d]) atomicAdd(&rowhist0[(size_t)pc * nbins0 + d], h[d]);
@@ -255,7 +256,8 @@ struct OsArgs {
     uint2* pout;           // (key, value) pairs, sorted by this pass's digit
     int n, shift, nbins, ntiles, nctas;
     uint32_t dmask;
-    const uint32_t* gofs;  // [nbins] exclusive scan of the digit totals
+    const uint32_t* gofs;  // [nbins] exclusive scan of the digit totals (first pass)
+    uint32_t* dtot;        // [nbins] later passes: the digit totals, from the column scans
     uint32_t* rowhist;     // [nctas][nbins] range histograms
     uint32_t* colpre;      // [nctas][nbins] their column-wise exclusive scans
     uint32_t* bar;         // grid-barrier arrival counter (zero at launch)
@@ -371,6 +373,7 @@ __global__ void __launch_bounds__(kRsThreads, ROUNDS >= 16 ? 2 : 3) os_pass_kern
             const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
             if (lane >= o) inc += v;
         }
+        if (UPSWEEP && lane == 31) a.dtot[d] = inc;  // the digit's total over all ranges
         uint32_t pre_ = inc - tot;
         for (int k = 0; k < per; k++) {
             const int r = lane * per + k;
@@ -382,8 +385,17 @@ __global__ void __launch_bounds__(kRsThreads, ROUNDS >= 16 ? 2 : 3) os_pass_kern
         }
     }
     grid_barrier(a.bar, 2u * (uint32_t)C);
-    // C. the range's tiles in order
-    for (int d = t; d < nbins; d += kRsThreads) boff[d] = a.gofs[d] + __ldcg(a.colpre + (size_t)c * nbins + d);
+    // C. the range's tiles in order, from running offsets = the digit's first position (the
+    // first pass: the convert's totals, scanned; later passes: the column totals of phase B,
+    // scanned here) + the column prefix of this range
+    if (UPSWEEP) {
+        for (int d = t; d < nbins; d += kRsThreads) boff[d] = __ldcg(a.dtot + d);
+        __syncthreads();
+        block_scan_smem(boff, nbins, s_ws);
+        for (int d = t; d < nbins; d += kRsThreads) boff[d] += __ldcg(a.colpre + (size_t)c * nbins + d);
+    } else {
+        for (int d = t; d < nbins; d += kRsThreads) boff[d] = a.gofs[d] + __ldcg(a.colpre + (size_t)c * nbins + d);
+    }
     uint16_t* my = wcnt + warp * nbins;
     const uint32_t lt = (1u << lane) - 1u;
     const bool pairs_in = a.pin != nullptr;
@@ -795,12 +807,13 @@ static int bin_sorted(kde_ctx* c, const double* d_x, const double* d_y, int n) {
         if (rc) return KDE_ENOMEM;
         pb.cap = cap;
     }
-    // hist: [passes][1025] totals, [passes][1025] their scans, a grid-barrier counter per pass
-    constexpr int kHistWords = 2 * kRsMaxPasses * kRsMaxDigits + kRsMaxPasses + 1;
+    // hist: [1025] first-pass digit totals, [1025] their scan, [passes][1025] later passes'
+    // totals (column scans), a grid-barrier counter per pass
+    constexpr int kHistWords = (2 + kRsMaxPasses) * kRsMaxDigits + kRsMaxPasses + 1;
     if (!pb.hist && grow((void**)&pb.hist, sizeof(uint32_t) * kHistWords)) return KDE_ENOMEM;
     uint32_t* ghist = pb.hist;
-    uint32_t* gofs = pb.hist + kRsMaxPasses * kRsMaxDigits;
-    uint32_t* bars = pb.hist + 2 * kRsMaxPasses * kRsMaxDigits;
+    uint32_t* gofs = pb.hist + kRsMaxDigits;  // then the later passes' totals (OsArgs::dtot)
+    uint32_t* bars = pb.hist + (2 + kRsMaxPasses) * kRsMaxDigits;
     // the passes' CTA count: every CTA resident (cooperative launch), at most one per tile
     const size_t dsmem = sizeof(uint2) * 2 * tile + sizeof(uint32_t) * 2 * nbins + sizeof(uint16_t) * 8 * nbins;
     auto k_first = rounds == 8 ? os_pass_kernel<8, false> : os_pass_kernel<16, false>;
@@ -827,7 +840,7 @@ static int bin_sorted(kde_ctx* c, const double* d_x, const double* d_y, int n) {
     }
     cudaMemsetAsync(c->d_stats, 0, 3 * sizeof(unsigned long long), s);
     if (n > 0) {
-        cudaMemsetAsync(ghist, 0, sizeof(uint32_t) * kRsMaxPasses * kRsMaxDigits, s);
+        cudaMemsetAsync(ghist, 0, sizeof(uint32_t) * kRsMaxDigits, s);
         cudaMemsetAsync(bars, 0, sizeof(uint32_t) * kRsMaxPasses, s);
         // the convert: each pass-0 range cut into `split` parts (~4 CTAs per SM), the parts'
         // digit counts added into the range histogram
@@ -836,7 +849,7 @@ static int bin_sorted(kde_ctx* c, const double* d_x, const double* d_y, int n) {
         bin_convert_kernel<<<nctas * split, kRsThreads, 0, s>>>(d_x, d_y, n, g, nb, pb.key[0], pb.rec, c->d_stats,
                                                                 passes, dbits, ghist, tile, nblk, pb.ost[0],
                                                                 pass_bins(0), split);
-        os_scan_kernel<<<passes, kRsThreads, 0, s>>>(ghist, gofs, dbits, passes, pass_bins(passes - 1));
+        os_scan_kernel<<<1, kRsThreads, 0, s>>>(ghist, gofs, dbits, passes, pass_bins(passes - 1));  // pass 0's
         c->launches += 2;
         int cur = 0;
         for (int ps = 0; ps < passes; ps++) {
@@ -851,7 +864,8 @@ static int bin_sorted(kde_ctx* c, const double* d_x, const double* d_y, int n) {
             oa.ntiles = nblk;
             oa.nctas = nctas;
             oa.dmask = pass_mask(ps);
-            oa.gofs = gofs + ps * kRsMaxDigits;
+            oa.gofs = gofs;                             // pass 0: the convert's totals, scanned
+            oa.dtot = gofs + (1 + ps) * kRsMaxDigits;  // later passes (ps >= 1): their column totals
             oa.rowhist = pb.ost[0];
             oa.colpre = pb.ost[1];
             oa.bar = bars + ps;
