@@ -159,9 +159,12 @@ KDE_API int kde_create(const kde_params* p, kde_ctx** out);
  *   x, y [in] n fp64 coordinates (world units), structure-of-arrays; either
  *             both host pointers (copied to the device through a pinned staging
  *             buffer) or both device pointers on params.device.  Not retained.
- *   n    [in] >= 0 (0 is legal: kde_eval then writes zeros).
+ *   n    [in] >= 0 (0 is legal: kde_eval then writes zeros); < 2^30 (the sort's counters;
+ *             KDE_EUNSUPPORTED otherwise).
  * Enqueues a1 (fp64 convert, integer support ranges, bucket keys) and a2 (stable
- * LSD counting sort by bucket key, gather to bucket-local fp32 SoA) on the
+ * LSD counting sort by bucket key -- one cooperative launch per radix pass, all of
+ * whose CTAs must be co-resident: a device shared with other work can refuse it,
+ * KDE_ECUDA -- and the gather to bucket-local fp32 SoA) on the
  * context's internal stream and returns without waiting for them (the integer
  * stats come back asynchronously; kde_get_stats waits).  Ordering: device
  * inputs are read after all work already queued on the legacy default stream
