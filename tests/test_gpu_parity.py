@@ -392,3 +392,23 @@ def test_tensor_fp16_range_cutoff9(hpx):
     assert _err(gpu, ref) <= TOL_TENSOR
     d = k.eval("direct").cpu().numpy()
     assert _err(d, ref) <= TOL_DIRECT
+
+
+@pytest.mark.parametrize("m64", ["1", "0"])
+@pytest.mark.parametrize("kernel", [6, 2])
+def test_tensor_tile_shapes_M64_and_M128(monkeypatch, m64, kernel):
+    """The tensor-core path's two tile shapes: M = 64 tiles (4-bucket stacks, two
+    accumulators per TMEM column slice, 16 workers) and M = 128 tiles (KDE_TC_M64=0: 12-bucket
+    stacks, 10 workers) on the same ragged, clustered input -- each against the oracle, and the
+    reported M matches the geometry."""
+    monkeypatch.setenv("KDE_TC_M64", m64)
+    c = case("estuary", 40_000, 200, 4.0, seed=83, H=170)
+    k = _kde(c, kernel=kernel)
+    k.load(torch.from_numpy(c["x"]).cuda(), torch.from_numpy(c["y"]).cuda())
+    gpu = k.eval("tensor").cpu().numpy()
+    st = k.stats()
+    k.close()
+    assert st["tc_m"] == (64 if m64 == "1" else 128)
+    assert st["main_kernel"] == 3  # the per-warp kernel (eval_tc5.cu) for both shapes
+    ref, _ = oracle.kde_raster(_grid(c, kernel=kernel), c["x"], c["y"], threads=THREADS)
+    assert _err(gpu, ref) <= TOL_TENSOR
