@@ -461,6 +461,94 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineArgs a) {
     }
 }
 
+// Combine pass for bucket-pitch groups (px = 8, one block per group): one CTA per 8-column
+// strip x 128 rows, each warp 8 columns x 16 rows (lane = column lane % 8, rows lane / 8 + 4k).
+// The strip is one bucket column wide, so a group window covers all of a warp's columns or
+// none (for F a multiple of 8; the column test stays for the rest), and a warp skips, as a
+// whole, every block whose rows miss its 16: each pixel adds only the blocks that can cover
+// it, in the list's order -- the same sum, bit for bit, as combine_kernel (the skipped blocks
+// add +0).
+constexpr int kStripH = 128, kStripEnt = 512;
+
+__global__ void __launch_bounds__(256) combine_strip_kernel(const CombineArgs a) {
+    __shared__ int4 s_ent[kStripEnt];
+    __shared__ int s_n;
+    const Geom& g = a.g;
+    const PathGeom& pg = a.pg;
+    const int X0 = blockIdx.x * 8, X1 = X0 + 7;
+    const int Y0 = g.rb + blockIdx.y * kStripH, Y1 = min(Y0 + kStripH, g.re) - 1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i = X0 + (lane & 7);
+    const int R0 = Y0 + 16 * warp;
+    {   // planner flags of the 32 x 32 tiles the strip meets: all clear -> zeros
+        const int tx = X0 / kCombTile, ty0 = (Y0 - g.rb) / kCombTile, ty1 = (Y1 - g.rb) / kCombTile;
+        const int tfx = (g.W + kCombTile - 1) / kCombTile;
+        bool any = false;
+        for (int ty = ty0; ty <= ty1; ty++) any |= a.tflag[(size_t)ty * tfx + tx] != 0;
+        if (!any) {
+            if (i < g.W)
+                for (int k = 0; k < 4; k++) {
+                    const int j = R0 + (lane >> 3) + 4 * k;
+                    if (j <= Y1) a.out[(size_t)(j - g.rb) * g.W + i] = 0.f;
+                }
+            return;
+        }
+    }
+    const int F = g.F;
+    const int gxa = max(floor_div(X0 - F, pg.px), 0), gxb = min(floor_div(X1 + F, pg.px), pg.ngx - 1);
+    const int gya = max(floor_div(Y0 - F, pg.py), 0), gyb = min(floor_div(Y1 + F, pg.py), pg.ngy - 1);
+    const int ngxr = gxb - gxa + 1, ng = ngxr * (gyb - gya + 1);
+    if (threadIdx.x < 32) {  // the blocks meeting the strip, group row-major (as combine_kernel)
+        int n = 0;
+        for (int gi0 = 0; gi0 < ng; gi0 += 32) {
+            const int gi = gi0 + lane;
+            const int gy = gya + gi / ngxr, gx = gxa + gi % ngxr;
+            int2 gr = make_int2(0, 0);
+            if (gi < ng) gr = a.group[gy * pg.ngx + gx];
+            const int wx0 = gx * pg.px - F, wy0 = gy * pg.py - F;
+            const bool meet = gi < ng && gr.y > 0 && X1 >= wx0 && X0 <= wx0 + pg.ww - 1 && Y1 >= wy0 &&
+                              Y0 <= wy0 + pg.wh - 1;
+            const unsigned m = __ballot_sync(0xffffffffu, meet);
+            if (meet) {
+                const int pos = n + __popc(m & ((1u << lane) - 1u));
+                if (pos < kStripEnt) s_ent[pos] = make_int4(gr.x, wx0, wy0, pg.ww | (pg.wh << 16));
+            }
+            n += __popc(m);
+        }
+        if (lane == 0) s_n = min(n, kStripEnt);
+    }
+    __syncthreads();
+    const int n = s_n;
+    const int sl = pg.slot_w;
+    const size_t sf = (size_t)pg.slot_floats();
+    const int r0 = lane >> 3;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int e = 0; e < n; e++) {
+        const int4 en = s_ent[e];
+        const int sh = en.w >> 16;
+        if (en.z > R0 + 15 || en.z + sh <= R0) continue;  // warp-uniform: the block misses its rows
+        const int li = i - en.y;
+        const bool inx = (unsigned)li < (unsigned)(en.w & 0xffff);
+        const float* sp = a.splat + (size_t)en.x * sf + li;
+        float v[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int lj = R0 + r0 + 4 * k - en.z;
+            v[k] = (inx && (unsigned)lj < (unsigned)sh) ? sp[(size_t)lj * sl] : 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; k++) acc[k] += v[k];
+    }
+    if (i >= g.W) return;
+    const unsigned long long nf = a.stats[0];
+    const float scale = nf ? (float)(a.c_over_h2 / (double)nf) : 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const int j = R0 + r0 + 4 * k;
+        if (j <= Y1) a.out[(size_t)(j - g.rb) * g.W + i] = acc[k] * scale;
+    }
+}
+
 template <int K, bool RAD, int TY, bool REC>
 static int launch_ty(const SplatArgs& a, int grid, cudaStream_t s) {
     const size_t smem = sizeof(float) * WLayout<TY>::SMEM_FLOATS;
@@ -528,8 +616,16 @@ int launch_combine(kde_ctx* c, const EvalPlan& pl, float* out, cudaStream_t s) {
     a.out = out;
     a.stats = c->d_stats;
     a.c_over_h2 = kernel_constant(c->kern, c->radial) / (c->hpx * c->hpx);
-    dim3 grid((g.W + kCombTile - 1) / kCombTile, (g.re - g.rb + kCombTile - 1) / kCombTile);
-    combine_kernel<<<grid, 256, 0, s>>>(a);
+    const PathGeom& pg = pl.pg;
+    const int strip_ent = ((8 + 2 * g.F) / pg.px + 2) * ((kStripH + 2 * g.F) / pg.py + 2);
+    static const bool env_strip = !getenv("KDE_COMBINE_STRIP") || atoi(getenv("KDE_COMBINE_STRIP")) != 0;
+    if (env_strip && pg.px == 8 && pg.nsub() == 1 && strip_ent <= kStripEnt) {
+        dim3 grid((g.W + 7) / 8, (g.re - g.rb + kStripH - 1) / kStripH);
+        combine_strip_kernel<<<grid, 256, 0, s>>>(a);
+    } else {
+        dim3 grid((g.W + kCombTile - 1) / kCombTile, (g.re - g.rb + kCombTile - 1) / kCombTile);
+        combine_kernel<<<grid, 256, 0, s>>>(a);
+    }
     c->launches += 1;
     return KDE_OK;
 }
