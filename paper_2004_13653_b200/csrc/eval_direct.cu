@@ -462,15 +462,18 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineArgs a) {
 }
 
 // Combine pass for bucket-pitch groups (px = 8, one block per group): one CTA per 8-column
-// strip x 128 rows, each warp 8 columns x 16 rows (lane = column lane % 8, rows lane / 8 + 4k).
+// strip x kStripH rows, each warp 8 columns x kStripH / 8 rows (lane = column lane % 8, rows
+// lane / 8 + 4k).
 // The strip is one bucket column wide, so a group window covers all of a warp's columns or
 // none (for F a multiple of 8; the column test stays for the rest), and a warp skips, as a
 // whole, every block whose rows miss its 16: each pixel adds only the blocks that can cover
 // it, in the list's order -- the same sum, bit for bit, as combine_kernel (the skipped blocks
 // add +0).
-constexpr int kStripH = 128, kStripEnt = 512;
+constexpr int kStripEnt = 512;
 
+template <int kStripH>  // rows per strip: 256 for tall group pitches (tensor path), else 128
 __global__ void __launch_bounds__(256) combine_strip_kernel(const CombineArgs a) {
+    constexpr int kStripRW = kStripH / 8, kStripK = kStripRW / 4;  // rows per warp, rows per thread
     __shared__ int4 s_ent[kStripEnt];
     __shared__ int s_n;
     const Geom& g = a.g;
@@ -479,7 +482,7 @@ __global__ void __launch_bounds__(256) combine_strip_kernel(const CombineArgs a)
     const int Y0 = g.rb + blockIdx.y * kStripH, Y1 = min(Y0 + kStripH, g.re) - 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int i = X0 + (lane & 7);
-    const int R0 = Y0 + 16 * warp;
+    const int R0 = Y0 + kStripRW * warp;
     {   // planner flags of the 32 x 32 tiles the strip meets: all clear -> zeros
         const int tx = X0 / kCombTile, ty0 = (Y0 - g.rb) / kCombTile, ty1 = (Y1 - g.rb) / kCombTile;
         const int tfx = (g.W + kCombTile - 1) / kCombTile;
@@ -487,7 +490,7 @@ __global__ void __launch_bounds__(256) combine_strip_kernel(const CombineArgs a)
         for (int ty = ty0; ty <= ty1; ty++) any |= a.tflag[(size_t)ty * tfx + tx] != 0;
         if (!any) {
             if (i < g.W)
-                for (int k = 0; k < 4; k++) {
+                for (int k = 0; k < kStripK; k++) {
                     const int j = R0 + (lane >> 3) + 4 * k;
                     if (j <= Y1) a.out[(size_t)(j - g.rb) * g.W + i] = 0.f;
                 }
@@ -522,28 +525,30 @@ __global__ void __launch_bounds__(256) combine_strip_kernel(const CombineArgs a)
     const int sl = pg.slot_w;
     const size_t sf = (size_t)pg.slot_floats();
     const int r0 = lane >> 3;
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    float acc[kStripK];
+#pragma unroll
+    for (int k = 0; k < kStripK; k++) acc[k] = 0.f;
     for (int e = 0; e < n; e++) {
         const int4 en = s_ent[e];
         const int sh = en.w >> 16;
-        if (en.z > R0 + 15 || en.z + sh <= R0) continue;  // warp-uniform: the block misses its rows
+        if (en.z > R0 + kStripRW - 1 || en.z + sh <= R0) continue;  // warp-uniform: the block misses its rows
         const int li = i - en.y;
         const bool inx = (unsigned)li < (unsigned)(en.w & 0xffff);
         const float* sp = a.splat + (size_t)en.x * sf + li;
-        float v[4];
+        float v[kStripK];
 #pragma unroll
-        for (int k = 0; k < 4; k++) {
+        for (int k = 0; k < kStripK; k++) {
             const int lj = R0 + r0 + 4 * k - en.z;
             v[k] = (inx && (unsigned)lj < (unsigned)sh) ? sp[(size_t)lj * sl] : 0.f;
         }
 #pragma unroll
-        for (int k = 0; k < 4; k++) acc[k] += v[k];
+        for (int k = 0; k < kStripK; k++) acc[k] += v[k];
     }
     if (i >= g.W) return;
     const unsigned long long nf = a.stats[0];
     const float scale = nf ? (float)(a.c_over_h2 / (double)nf) : 0.f;
 #pragma unroll
-    for (int k = 0; k < 4; k++) {
+    for (int k = 0; k < kStripK; k++) {
         const int j = R0 + r0 + 4 * k;
         if (j <= Y1) a.out[(size_t)(j - g.rb) * g.W + i] = acc[k] * scale;
     }
@@ -617,11 +622,15 @@ int launch_combine(kde_ctx* c, const EvalPlan& pl, float* out, cudaStream_t s) {
     a.stats = c->d_stats;
     a.c_over_h2 = kernel_constant(c->kern, c->radial) / (c->hpx * c->hpx);
     const PathGeom& pg = pl.pg;
-    const int strip_ent = ((8 + 2 * g.F) / pg.px + 2) * ((kStripH + 2 * g.F) / pg.py + 2);
+    // strips of 256 rows when the group pitch is tall (tensor-core stacks: fewer block lists
+    // per pixel), else 128 (measured: C4 tensor 0.174 -> 0.167 ms at 256, direct 0.255 -> 0.264)
+    const int sh = pg.py >= 32 ? 256 : 128;
+    const int strip_ent = ((8 + 2 * g.F) / pg.px + 2) * ((sh + 2 * g.F) / pg.py + 2);
     static const bool env_strip = !getenv("KDE_COMBINE_STRIP") || atoi(getenv("KDE_COMBINE_STRIP")) != 0;
     if (env_strip && pg.px == 8 && pg.nsub() == 1 && strip_ent <= kStripEnt) {
-        dim3 grid((g.W + 7) / 8, (g.re - g.rb + kStripH - 1) / kStripH);
-        combine_strip_kernel<<<grid, 256, 0, s>>>(a);
+        dim3 grid((g.W + 7) / 8, (g.re - g.rb + sh - 1) / sh);
+        if (sh == 256) combine_strip_kernel<256><<<grid, 256, 0, s>>>(a);
+        else combine_strip_kernel<128><<<grid, 256, 0, s>>>(a);
     } else {
         dim3 grid((g.W + kCombTile - 1) / kCombTile, (g.re - g.rb + kCombTile - 1) / kCombTile);
         combine_kernel<<<grid, 256, 0, s>>>(a);
