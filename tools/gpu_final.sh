@@ -19,7 +19,7 @@ for c in C2 C4; do timeout 300 python bench.py --config $c --path snap --steps 1
 timeout 900 python tools/band_projection.py --config C4 --path tensor > $F/band_projection_c4.jsonl 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $F/launches_c4_tensor.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $F/launches_c4_direct.csv python bench.py --path direct --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tc5_kernel|combine_kernel|os_pass_kernel|bin_convert|gather_offsets" -c 6 -o $F/c4_tensor -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tc5_kernel|combine_strip_kernel|combine_kernel|os_pass_kernel|bin_convert|gather_offsets" -c 6 -o $F/c4_tensor -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^splat_kernel|segreduce" -c 2 -o $F/c4_direct -f python bench.py --path direct --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 for f in paper_2004_13653_b200/build/*.o; do echo "== $f"; cuobjdump -sass $f | grep -oE "UTCHMMA|UTCBAR|LDTM|UTMALDG|UBLKCP|FFMA2|FMUL2|FFMA |MUFU.EX2|SYNCS[.A-Z]*" | sort | uniq -c; done > $F/sass_counts.txt 2>&1
 ls -la $F
