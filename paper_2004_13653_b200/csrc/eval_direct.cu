@@ -626,7 +626,8 @@ int launch_combine(kde_ctx* c, const EvalPlan& pl, float* out, cudaStream_t s) {
     // per pixel), else 128 (measured: C4 tensor 0.174 -> 0.167 ms at 256, direct 0.255 -> 0.264)
     const int sh = pg.py >= 32 ? 256 : 128;
     const int strip_ent = ((8 + 2 * g.F) / pg.px + 2) * ((sh + 2 * g.F) / pg.py + 2);
-    static const bool env_strip = !getenv("KDE_COMBINE_STRIP") || atoi(getenv("KDE_COMBINE_STRIP")) != 0;
+    const char* env_s = getenv("KDE_COMBINE_STRIP");  // 0: the 32 x 32-tile kernel (tests, A/B)
+    const bool env_strip = !env_s || atoi(env_s) != 0;
     if (env_strip && pg.px == 8 && pg.nsub() == 1 && strip_ent <= kStripEnt) {
         dim3 grid((g.W + 7) / 8, (g.re - g.rb + sh - 1) / sh);
         if (sh == 256) combine_strip_kernel<256><<<grid, 256, 0, s>>>(a);

@@ -412,3 +412,23 @@ def test_tensor_tile_shapes_M64_and_M128(monkeypatch, m64, kernel):
     assert st["main_kernel"] == 3  # the per-warp kernel (eval_tc5.cu) for both shapes
     ref, _ = oracle.kde_raster(_grid(c, kernel=kernel), c["x"], c["y"], threads=THREADS)
     assert _err(gpu, ref) <= TOL_TENSOR
+
+
+@pytest.mark.parametrize("path", ["tensor", "direct"])
+def test_strip_combine_bitwise_equals_tile_combine(monkeypatch, path):
+    """The strip combine (8-column strips, warp-uniform block skipping) adds the same blocks in
+    the same order as the 32 x 32-tile combine: bitwise-identical rasters on a clustered input
+    with ragged raster edges (combine pass round 2)."""
+    c = case("estuary", 60_000, 260, 4.0, seed=91, H=230)
+
+    def run(strip):
+        monkeypatch.setenv("KDE_COMBINE_STRIP", strip)
+        k = _kde(c, kernel=6)
+        k.load(torch.from_numpy(c["x"]).cuda(), torch.from_numpy(c["y"]).cuda())
+        out = k.eval(path).cpu().numpy()
+        k.close()
+        return out
+
+    a, b = run("1"), run("0")
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    assert a.max() > 0
