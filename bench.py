@@ -430,7 +430,11 @@ def run_ours(args):
                 "executed_mma_flops_per_launch": mma,
                 "executed_mma_tflops": round(mma / (eval_ms * 1e-3) / 1e12, 3),
                 "executed_frac": float(f"{mma / (eval_ms * 1e-3) / 1e12 / peak:.4g}"),
-                "useful_share_of_mma": round(2.0 * st["useful_pairs"] / max(mma, 1), 4)}
+                "useful_share_of_mma": round(2.0 * st["useful_pairs"] / max(mma, 1), 4),
+                # context for BASELINE's north star, which names a tf32 path: the same useful
+                # TFLOP/s against the tf32 dense rate (1.1 of 2.25 PFLOP/s nominal: x 0.489 of
+                # the measured bf16 peak; B200_PROFILING.md)
+                "frac_vs_tf32_peak": float(f"{useful_tf / (peak * 1.1 / 2.25):.4g}")}
     roof["frac"] = float(f"{roof['achieved'] / roof['peak']:.4g}")
     roof["achieved"] = float(f"{roof['achieved']:.6g}")
     roof["traffic"] = _traffic(f"{_workload_key(args)}/{path}/{roof['kernel']}")
